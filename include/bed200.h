@@ -1,0 +1,109 @@
+/*
+ * bed200.h -- C ABI of the B200-native batched symmetric eigendecomposition
+ * (arXiv 2207.04228: Householder tridiagonalisation + double-Wilkinson-shift
+ * Givens QR with per-matrix deflation, eigenvector accumulation, and the
+ * Taylor-polynomial ED backward).
+ *
+ * Plain pointers and sizes only.  Device entry points take device pointers
+ * and a CUDA stream (cudaStream_t passed as void*), are asynchronous and
+ * stream-ordered, allocate nothing and keep no global mutable state
+ * (reentrant; one call per device stream).  The host entry point takes host
+ * pointers and does the copies itself.
+ *
+ * Reference interfaces each entry point replaces (paths relative to the
+ * reference package root /root/reference/pkg/src/batchedeig):
+ *
+ *   bed_forward_f32        batched_eig()            solver.py:79-112
+ *                          = validate               core.py:286-309
+ *                          + tridiagonalize_kernel  _kernels.py:36-92
+ *                            (values-only: reduce_band_kernel _kernels.py:95-202)
+ *                          + qr_loop_kernel         _kernels.py:321-398
+ *                          + finalize_kernel        _kernels.py:401-417
+ *                          + accumulate_reflectors / wy_accumulate
+ *                                                   householder.py:216-271
+ *                          + V = P @ Q              solver.py:93
+ *                          + _sort_and_sign         solver.py:60-76
+ *   bed_forward_host_f32   the same call on host (numpy-side) buffers, the
+ *                          way the reference API is called (solver.py:79)
+ *   bed_backward_f32       (absent in the reference: pkg/README.md:116-117)
+ *                          ED backward with Taylor-K
+ *   bed_error_string       error text for the integer return codes; the
+ *                          reference maps kernel status ints to exceptions
+ *                          in qr.py:604-609 / oracle.py:76-79
+ */
+#ifndef BED200_H_
+#define BED200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BED200_ABI_VERSION 1
+
+/* Return codes of every entry point. */
+#define BED_SUCCESS 0
+#define BED_ERR_INVALID_ARGUMENT 1 /* null pointer, n out of [1, 64], batch < 0, bad enum */
+#define BED_ERR_MISALIGNED 2       /* device pointer not 16-byte aligned */
+#define BED_ERR_CUDA 3             /* launch / runtime failure (see bed_last_cuda_error) */
+#define BED_ERR_NO_DEVICE 4        /* no sm_100 device visible */
+
+/* Per-matrix numerical status (written to `status`), mirroring the
+ * reference exceptions NoConvergence / NonFinite / NonSymmetric
+ * (core.py:46-93). */
+#define BED_STATUS_OK 0
+#define BED_STATUS_NO_CONVERGENCE 1 /* budget exhausted, a coupling >= deflation_tol remains */
+#define BED_STATUS_NON_FINITE 2     /* NaN/Inf in the input matrix */
+#define BED_STATUS_NON_SYMMETRIC 3  /* max|a_ij-a_ji| > symmetry_tol * max(1, ||A||_F) */
+
+#define BED_SORT_NONE 0
+#define BED_SORT_DESCENDING 1
+#define BED_SORT_ASCENDING 2
+
+/* SolverConfig (core.py:226-279) as the kernels see it. */
+typedef struct bed_config {
+  float deflation_tol;      /* absolute, on the power-of-two equilibrated band (qr.py:512-515) */
+  float symmetry_tol;       /* relative asymmetry tolerance (core.py:254) */
+  int32_t max_double_steps; /* <= 0 resolves to 2n (core.py:270-271) */
+  int32_t sort;             /* BED_SORT_* */
+  int32_t compute_vectors;  /* 0: eigenvalues only (solver.py:94-109) */
+  int32_t reserved;         /* must be 0 */
+} bed_config;
+
+/* Forward: A (batch, n, n) row-major FP32, symmetrised on load.
+ *   evals  (batch, n)            required
+ *   evecs  (batch, n, n)         required iff compute_vectors; column j pairs with evals[:, j]
+ *   status (batch) int32         nullable; BED_STATUS_*
+ *   steps  (batch) int32         nullable; double-shift steps this matrix used
+ *   flags  (1) int32             nullable; set to OR over matrices of (1 << status)
+ * Eigenvalues are ordered per cfg->sort and every eigenvector column is sign
+ * normalised so its largest-magnitude entry (first on ties) is >= 0.
+ * All pointers are device pointers; `stream` is a cudaStream_t (NULL = legacy default). */
+int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
+                    int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
+                    void* stream);
+
+/* Same computation on HOST buffers (pinned or pageable), on CUDA device
+ * `device`.  Streams the batch through the GPU in chunks with copies
+ * overlapped against compute; returns after the results are on the host. */
+int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
+                         int32_t* status, int32_t* steps, const bed_config* cfg, int32_t device);
+
+/* Backward with the Taylor-polynomial K of degree `taylor_degree` (paper: 9):
+ *   gA = sym( V (F o (V^T gV) + diag(gL)) V^T ),  sym(M) = (M + M^T)/2,
+ *   F_ij ~ 1/(l_j - l_i) via (1/l_big) sum_{k=0..degree} (l_small/l_big)^k.
+ * V (batch,n,n), evals (batch,n) as returned by bed_forward_f32; gV and gL
+ * are nullable (zero cotangent); gA (batch,n,n) is written. Device pointers. */
+int bed_backward_f32(const float* V, const float* evals, const float* gV, const float* gL,
+                     float* gA, int64_t batch, int32_t n, int32_t taylor_degree, void* stream);
+
+const char* bed_error_string(int code);
+const char* bed_last_cuda_error(void); /* thread-local text of the last BED_ERR_CUDA */
+int bed_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BED200_H_ */

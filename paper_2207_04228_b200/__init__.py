@@ -1,0 +1,32 @@
+"""B200-native batched symmetric eigendecomposition (arXiv 2207.04228).
+
+Drop-in for the reference ``batchedeig`` forward API on the GPU (same
+names: ``batched_eig``, ``SolverConfig``, ``EigenResult``, ``BatchedSymmetric``
+and the error types), plus the differentiable ``eigh`` / ``BatchedEigFn``
+with the paper's Taylor-polynomial backward.  All compute runs in the
+sm_100a kernels of ``_lib/libbed200.so`` (C ABI: ``include/bed200.h``).
+"""
+
+from .core import (  # noqa: F401
+    BatchedEigError,
+    BatchedSymmetric,
+    EigenResult,
+    NoConvergence,
+    NonFinite,
+    NonPositiveSpectrum,
+    NonSymmetric,
+    ShapeMismatch,
+    SolveDiagnostics,
+    SolverConfig,
+)
+from .solver import (  # noqa: F401
+    TAYLOR_DEGREE,
+    BatchedEigFn,
+    batched_eig,
+    eigh,
+    forward_into,
+    taylor_backward,
+)
+from .sharding import gather_shards, shard_bounds, shard_sizes, solve_shard  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,37 @@
+// Instantiations of the Taylor-K backward kernel.
+#include "bed_backward.cuh"
+#include "bed_launch.h"
+
+namespace bed {
+
+template <int NMAX, bool EXACT>
+static cudaError_t go_bwd(const BwdArgs& a) {
+  using P = BwdParams<NMAX>;
+  auto kern = bed_backward_kernel<NMAX, EXACT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const unsigned grid = (unsigned)((a.batch + P::MB - 1) / P::MB);
+  kern<<<grid, P::THREADS, P::BYTES, a.stream>>>(a.V, a.lam, a.gV, a.gL, a.gA, a.batch, a.n,
+                                                 a.degree);
+  return cudaGetLastError();
+}
+
+template <int NMAX>
+static cudaError_t go_bwd_n(const BwdArgs& a) {
+  return a.n == NMAX ? go_bwd<NMAX, true>(a) : go_bwd<NMAX, false>(a);
+}
+
+cudaError_t launch_backward(const BwdArgs& a) {
+  if (a.n <= 4) return go_bwd_n<4>(a);
+  if (a.n <= 8) return go_bwd_n<8>(a);
+  if (a.n <= 16) return go_bwd_n<16>(a);
+  if (a.n <= 32) return go_bwd_n<32>(a);
+  return go_bwd_n<64>(a);
+}
+
+}  // namespace bed

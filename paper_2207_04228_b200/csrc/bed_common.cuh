@@ -1,0 +1,133 @@
+// bed_common.cuh -- scalar building blocks shared by the forward kernels.
+//
+// Each helper restates one reference primitive in FP32 (the reference is
+// float64 numba; /root/reference/pkg/src/batchedeig/...):
+//   givens()     rotation generation of _sweep_block, _kernels.py:244-258
+//                (zero target -> identity rotation exactly, :247, :256-258)
+//   wilkinson()  _wilkinson_scalar, _kernels.py:205-218 (mu_hi is the root
+//                nearer the trailing entry, applied first: qr.py:67-76)
+//   pow2_ceil()  _band_scale, qr.py:522-534 (exact power-of-two equilibration)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#define BED_HD __host__ __device__ __forceinline__
+
+namespace bed {
+
+constexpr int kStatusOk = 0;
+constexpr int kStatusNoConv = 1;
+constexpr int kStatusNonFinite = 2;
+constexpr int kStatusNonSym = 3;
+
+// Column tails at or below this are already reduced (householder.py:37-39
+// uses 1e-300 in float64; this is the FP32 analogue, well above the
+// denormal range so 1/scale stays finite).
+constexpr float kZeroTail = 1e-30f;
+
+struct KernelCfg {
+  float eps;       // deflation_tol
+  float sym_tol;   // symmetry_tol
+  int max_steps;   // resolved double-step budget
+  int sort;        // 0 none, 1 descending, 2 ascending
+};
+
+BED_HD float rsqrt_approx(float x) {
+#ifdef __CUDA_ARCH__
+  return rsqrtf(x);
+#else
+  return 1.0f / sqrtf(x);
+#endif
+}
+
+// 1/sqrt(x) refined by one Newton step (MUFU.RSQ is ~2 ulp; the refined
+// value keeps c^2 + s^2 within an ulp of 1 so V stays orthogonal over the
+// thousands of rotations an n=64 solve folds).
+BED_HD float rsqrt_nr(float x) {
+  float y = rsqrt_approx(x);
+  float hx = 0.5f * x;
+  return y * fmaf(-hx * y, y, 1.5f);
+}
+
+// Givens rotation annihilating e against dw: R^T (dw, e) = (r, 0) with
+// R = [[c, s], [-s, c]] (tests/helpers.py:14-22 convention, s = -e/r).
+BED_HD void givens(float dw, float e, float& c, float& s, float& r) {
+  if (e == 0.0f) {
+    c = 1.0f;
+    s = 0.0f;
+    r = dw;
+    return;
+  }
+  float h2 = fmaf(dw, dw, e * e);
+  if (h2 > 1e-30f && h2 < 1e30f) {
+    float ih = rsqrt_nr(h2);
+    c = dw * ih;
+    s = -e * ih;
+    r = h2 * ih;
+  } else {  // branch-scaled form of the reference (_kernels.py:248-258)
+    float am = fmaxf(fabsf(dw), fabsf(e));
+    float iam = 1.0f / am;
+    float t1 = dw * iam, t2 = e * iam;
+    float hh2 = fmaf(t1, t1, t2 * t2);
+    float ih = rsqrt_nr(hh2);
+    c = t1 * ih;
+    s = -t2 * ih;
+    r = am * (hh2 * ih);
+  }
+}
+
+// Eigenvalue pair of [[a, b], [b, d]] plus its diagonalising rotation.
+BED_HD void wilkinson(float a, float b, float d, float& lo, float& hi, float& c, float& s) {
+  if (b == 0.0f) {
+    lo = a;
+    hi = d;
+    c = 1.0f;
+    s = 0.0f;
+    return;
+  }
+  float m = (a - d) / (2.0f * b);
+  float sign = m >= 0.0f ? 1.0f : -1.0f;
+  float am = fabsf(m);
+  float root = am > 1e18f ? am : sqrtf(fmaf(m, m, 1.0f));  // hypot(1, m)
+  float t = -sign / (am + root);
+  c = 1.0f / sqrtf(fmaf(t, t, 1.0f));
+  s = c * t;
+  float bcs2 = 2.0f * b * c * s;
+  lo = (a * c * c - bcs2) + d * s * s;
+  hi = (a * s * s + bcs2) + d * c * c;
+}
+
+// 2^ceil(log2(top)) for top > 0 (1 for top == 0), computed exactly.
+BED_HD float pow2_ceil(float top) {
+  if (!(top > 0.0f)) return 1.0f;
+  int ex;
+  float f = frexpf(top, &ex);  // top = f * 2^ex, f in [0.5, 1)
+  if (f == 0.5f) ex -= 1;
+  return ldexpf(1.0f, ex);
+}
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).  Used
+// where a loop index must be a constant so register arrays stay in
+// registers -- the NVVM unroller gives up on very large bodies (the n = 64
+// reduction), template expansion never does.
+template <int B, int E, typename F>
+BED_HD void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+// Stable rank of slot c among n values for the requested order: the
+// position _sort_and_sign (solver.py:60-76) moves slot c to.
+BED_HD bool rank_before(float kv, int kidx, float v, int idx, int sort) {
+  // does (kv, kidx) sort strictly before (v, idx)?
+  if (sort == 1) return kv > v || (kv == v && kidx < idx);
+  return kv < v || (kv == v && kidx < idx);
+}
+
+}  // namespace bed

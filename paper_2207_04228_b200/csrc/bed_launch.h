@@ -1,0 +1,43 @@
+// bed_launch.h -- internal launcher interface between the C ABI
+// (bed_capi.cu) and the per-size kernel instantiation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bed_common.cuh"
+
+namespace bed {
+
+struct FwdArgs {
+  const float* A;
+  int64_t batch;
+  int n;
+  float* evals;
+  float* evecs;  // null => values only
+  int32_t* status;
+  int32_t* steps;
+  int32_t* flags;
+  KernelCfg cfg;
+  cudaStream_t stream;
+};
+
+struct BwdArgs {
+  const float* V;
+  const float* lam;
+  const float* gV;
+  const float* gL;
+  float* gA;
+  int64_t batch;
+  int n;
+  int degree;
+  cudaStream_t stream;
+};
+
+cudaError_t launch_small(const FwdArgs& a);      // 1 <= n <= 8   (bed_small.cu)
+cudaError_t launch_medium16(const FwdArgs& a);   // 9 <= n <= 16  (bed_medium16.cu)
+cudaError_t launch_medium32(const FwdArgs& a);   // 17 <= n <= 32 (bed_medium32.cu)
+cudaError_t launch_medium64(const FwdArgs& a);   // 33 <= n <= 64 (bed_medium64.cu)
+cudaError_t launch_backward(const BwdArgs& a);   // 1 <= n <= 64  (bed_backward.cu)
+
+}  // namespace bed

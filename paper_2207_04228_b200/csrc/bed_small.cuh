@@ -1,0 +1,355 @@
+// bed_small.cuh -- forward ED for n <= 8: one thread owns one matrix.
+//
+// Layout: a CTA of 128 threads solves 128 consecutive matrices.  The tile
+// (128 * n^2 floats, contiguous in HBM) is staged through shared memory
+// with coalesced 128-bit loads into an odd per-matrix stride, so every
+// thread's private reads are bank-conflict free; outputs leave the same
+// way.  Everything else -- the symmetric lower triangle, the band, V and
+// the loop state -- lives in registers; every array index is a
+// compile-time constant (loops fully unrolled on N, the per-matrix active
+// size m is a runtime predicate), so nothing spills to local memory.
+//
+// Per-matrix pipeline (reference /root/reference/pkg/src/batchedeig):
+//   validate + symmetrise        core.py:286-309
+//   Householder reduction        _kernels.py:36-92, with V <- V H_i folded
+//                                in as each reflector is made (= P of
+//                                householder.py:216-231, V starts as P so
+//                                V = P Q of solver.py:93 needs no GEMM)
+//   power-of-two equilibration   qr.py:522-534, :596-598, :624
+//   double-shift QR loop         _kernels.py:321-398 with the deflation
+//                                gate applied per matrix (the reference's
+//                                own per-matrix bookkeeping :381-388)
+//   fused sweep                  _kernels.py:221-300
+//   2x2 closeout                 _kernels.py:401-417
+//   sort + sign                  solver.py:60-76
+#pragma once
+
+#include "bed_common.cuh"
+
+namespace bed {
+
+constexpr int kSmallThreads = 128;
+
+template <int N>
+struct SmallLayout {
+  static constexpr int NN = N * N;
+  static constexpr int STRIDE = (NN % 2) ? NN : NN + 1;  // odd => conflict free
+  static constexpr int LSTRIDE = (N % 2) ? N : N + 1;
+};
+
+// A(r, c) of the symmetric lower-triangle store.
+template <int N>
+BED_HD float sym_at(const float (&a)[N][N], int r, int c) {
+  return c <= r ? a[r][c] : a[c][r];
+}
+
+template <int N, bool VECS>
+BED_HD void small_fold(float (&v)[N][N], int p, float c, float s) {
+  if constexpr (VECS) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      float x = v[r][p], y = v[r][p + 1];
+      v[r][p] = c * x - s * y;
+      v[r][p + 1] = s * x + c * y;
+    }
+  }
+}
+
+// One explicit shifted QR sweep of the leading m-block, fused exactly like
+// _sweep_block (rotation i-1 retires once rotation i exists).  Written as
+// straight-line predicated code over all N positions: rotations at
+// positions >= m-1 degenerate to the identity (a zero target gives c=1,
+// s=0 exactly, _kernels.py:247) and writes past the active block are
+// masked with selects.  Control flow that depends on m would let the
+// compiler merge the per-position blocks into one dynamically indexed block,
+// which demotes d, e and V to local memory.
+template <int N, bool VECS>
+BED_HD void small_sweep(float (&d)[N], float (&e)[N], float (&v)[N][N], int m, float mu) {
+  float dw = d[0] - mu, g = e[0];
+  float c1 = 1.0f, s1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool act = i < m - 1;
+    const float ei = (i < N - 1 && act) ? e[i] : 0.0f;
+    float c, s, r;
+    givens(dw, ei, c, s, r);
+    const float dn = (i + 1 < N ? d[i + 1] : 0.0f) - mu;
+    const float un = c * g - s * dn;
+    const float dwn = fmaf(s, g, c * dn);
+    if (i > 0) {
+      const bool wr = i <= m - 1;  // rotation i-1 was a real one
+      const float dret = (c1 * (c2 * r1) - s1 * u1) + mu;
+      d[i - 1] = wr ? dret : d[i - 1];
+      e[i - 1] = wr ? -s1 * r : e[i - 1];
+      small_fold<N, VECS>(v, i - 1, c1, s1);  // identity once past the block
+    }
+    if (i == m - 1) d[i] = c1 * dw + mu;
+    c2 = c1;
+    c1 = c;
+    s1 = s;
+    r1 = r;
+    u1 = un;
+    dw = dwn;
+    if (i + 1 < N - 1) g = c1 * e[i + 1];
+  }
+}
+
+// Trailing deflation: while m > 2 and |e[m-2]| < eps, m -= 1 -- on a bit
+// mask of the small couplings, so no array is indexed by m.
+template <int N>
+BED_HD int small_deflate(const float (&e)[N], int m, float eps) {
+  unsigned small = 0;
+#pragma unroll
+  for (int j = 0; j < N - 1; ++j) small |= (fabsf(e[j]) < eps ? 1u : 0u) << j;
+  while (m > 2 && ((small >> (m - 2)) & 1u)) --m;
+  return m;
+}
+
+template <int N, bool VECS>
+__global__ void __launch_bounds__(kSmallThreads)
+    bed_small_kernel(const float* __restrict__ A, int64_t batch, float* __restrict__ evals,
+                     float* __restrict__ evecs, int32_t* __restrict__ status_out,
+                     int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg) {
+  using Lay = SmallLayout<N>;
+  constexpr int NN = Lay::NN;
+  __shared__ float tile[kSmallThreads * Lay::STRIDE];
+  __shared__ float ltile[kSmallThreads * Lay::LSTRIDE];
+
+  const int64_t base = (int64_t)blockIdx.x * kSmallThreads;
+  const int count = (batch - base) < kSmallThreads ? (int)(batch - base) : kSmallThreads;
+  const int tid = threadIdx.x;
+  const bool live = tid < count;
+
+  // ---- coalesced tile load (128-bit when the tile is 16-byte aligned)
+  {
+    const float* src = A + base * NN;
+    const int total = count * NN;
+    if ((NN % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+      const float4* src4 = reinterpret_cast<const float4*>(src);
+      for (int g4 = tid; g4 < total / 4; g4 += kSmallThreads) {
+        float4 x = __ldg(src4 + g4);
+        int g = 4 * g4;
+        int mat = g / NN, off = g % NN;
+        float* dst = tile + mat * Lay::STRIDE + off;  // NN%4==0: no row straddle
+        dst[0] = x.x; dst[1] = x.y; dst[2] = x.z; dst[3] = x.w;
+      }
+    } else {
+      for (int g = tid; g < total; g += kSmallThreads)
+        tile[(g / NN) * Lay::STRIDE + (g % NN)] = __ldg(src + g);
+    }
+  }
+  __syncthreads();
+
+  // ---- validate + symmetrise (core.py:286-309)
+  float a[N][N];
+  int status = kStatusOk;
+  {
+    const float* my = tile + tid * Lay::STRIDE;
+    float x[N][N];
+    bool finite = true;
+    float fro2 = 0.0f, asym = 0.0f;
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        x[r][c] = live ? my[r * N + c] : 0.0f;
+        finite = finite && isfinite(x[r][c]);
+        fro2 = fmaf(x[r][c], x[r][c], fro2);
+      }
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) asym = fmaxf(asym, fabsf(x[r][c] - x[c][r]));
+    float limit = cfg.sym_tol * fmaxf(1.0f, sqrtf(fro2));
+    if (!finite) status = kStatusNonFinite;
+    else if (asym > limit) status = kStatusNonSym;
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c)
+        a[r][c] = status == kStatusOk ? 0.5f * (x[r][c] + x[c][r]) : 0.0f;
+  }
+
+  // ---- Householder tridiagonalisation with V <- V H_i accumulated in place
+  float v[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) v[r][c] = (VECS && r == c) ? 1.0f : 0.0f;
+
+#pragma unroll
+  for (int i = 0; i < N - 2; ++i) {
+    float scale = 0.0f;
+#pragma unroll
+    for (int r = i + 1; r < N; ++r) scale = fmaxf(scale, fabsf(a[r][i]));
+    if (scale > kZeroTail) {
+      float is = 1.0f / scale;
+      float sumsq = 0.0f;
+#pragma unroll
+      for (int r = i + 1; r < N; ++r) {
+        float t = a[r][i] * is;
+        sumsq = fmaf(t, t, sumsq);
+      }
+      float norm = scale * sqrtf(sumsq);
+      float pivot = a[i + 1][i];
+      float sigma = pivot >= 0.0f ? norm : -norm;
+      float u0 = pivot + sigma;
+      float iu = 1.0f / (sqrtf(2.0f * fabsf(sigma)) * sqrtf(fabsf(u0)));
+      float u[N];
+#pragma unroll
+      for (int r = 0; r < N; ++r) u[r] = r <= i ? 0.0f : (r == i + 1 ? u0 : a[r][i]) * iu;
+      // p = 2 A u on rows i.., K = u^T p, q = p - K u  (u_i = 0)
+      float q[N];
+      float kk = 0.0f;
+#pragma unroll
+      for (int r = i; r < N; ++r) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = i + 1; c < N; ++c) acc = fmaf(sym_at<N>(a, r, c), u[c], acc);
+        q[r] = 2.0f * acc;
+        if (r > i) kk = fmaf(u[r], q[r], kk);
+      }
+#pragma unroll
+      for (int r = i + 1; r < N; ++r) q[r] = fmaf(-kk, u[r], q[r]);
+      // A <- A - q u^T - u q^T on the trailing lower triangle
+#pragma unroll
+      for (int r = i; r < N; ++r)
+#pragma unroll
+        for (int c = i; c <= r; ++c) a[r][c] -= fmaf(q[r], u[c], u[r] * q[c]);
+      if constexpr (VECS) {
+        // V <- V (I - 2 u u^T): columns before i+1 are untouched
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          float t = 0.0f;
+#pragma unroll
+          for (int c = i + 1; c < N; ++c) t = fmaf(v[r][c], u[c], t);
+          t *= 2.0f;
+#pragma unroll
+          for (int c = i + 1; c < N; ++c) v[r][c] = fmaf(-t, u[c], v[r][c]);
+        }
+      }
+    }
+  }
+
+  // ---- band, equilibration
+  float d[N], e[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    d[j] = a[j][j];
+    e[j] = j + 1 < N ? a[j + 1][j] : 0.0f;
+  }
+  float top = 0.0f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) top = fmaxf(top, fmaxf(fabsf(d[j]), fabsf(e[j])));
+  const float scale = pow2_ceil(top);
+  const float iscale = 1.0f / scale;  // exact: power of two
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    d[j] *= iscale;
+    e[j] *= iscale;
+  }
+
+  // ---- double-shift QR with per-matrix deflation
+  int steps = 0;
+  if constexpr (N >= 3) {
+    int m = small_deflate<N>(e, N, cfg.eps);
+    while (m > 2) {
+      if (steps >= cfg.max_steps) {
+        float resid = 0.0f;
+#pragma unroll
+        for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
+        if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
+        break;  // lock the diagonal; the leading 2x2 still closes below
+      }
+      // trailing 2x2 of the active block; an arithmetic blend, not a select
+      // chain, so the compiler cannot fold it into a dynamically indexed
+      // (local-memory) load of d[m-2]
+      float ta = 0.0f, tb = 0.0f, td = 0.0f;
+#pragma unroll
+      for (int j = 1; j < N - 1; ++j) {
+        const float w = (j == m - 2) ? 1.0f : 0.0f;
+        ta = fmaf(w, d[j], ta);
+        tb = fmaf(w, e[j], tb);
+        td = fmaf(w, d[j + 1], td);
+      }
+      float lo, hi, wc, ws;
+      wilkinson(ta, tb, td, lo, hi, wc, ws);
+      small_sweep<N, VECS>(d, e, v, m, hi);
+      m = small_deflate<N>(e, m, cfg.eps);
+      if (m > 2) {
+        small_sweep<N, VECS>(d, e, v, m, lo);
+        m = small_deflate<N>(e, m, cfg.eps);
+      }
+      ++steps;
+    }
+  }
+  if constexpr (N >= 2) {
+    float lo, hi, c, s;
+    wilkinson(d[0], e[0], d[1], lo, hi, c, s);
+    d[0] = lo;
+    d[1] = hi;
+    small_fold<N, VECS>(v, 0, c, s);
+  }
+
+  // ---- sort (stable) + sign, staged back through shared memory
+  int rank[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    int rk = 0;
+    if (cfg.sort != 0) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) rk += (k != c && rank_before(d[k], k, d[c], c, cfg.sort)) ? 1 : 0;
+    } else {
+      rk = c;
+    }
+    rank[c] = rk;
+  }
+  __syncthreads();  // every thread is done reading its input tile
+  if (live) {
+    float* lrow = ltile + tid * Lay::LSTRIDE;
+#pragma unroll
+    for (int c = 0; c < N; ++c) lrow[rank[c]] = d[c] * scale;
+    if constexpr (VECS) {
+      float* my = tile + tid * Lay::STRIDE;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        float best = -1.0f, lead = 0.0f;
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          float mag = fabsf(v[r][c]);
+          if (mag > best) { best = mag; lead = v[r][c]; }
+        }
+        float flip = lead < 0.0f ? -1.0f : 1.0f;
+#pragma unroll
+        for (int r = 0; r < N; ++r) my[r * N + rank[c]] = v[r][c] * flip;
+      }
+    }
+    if (status_out) status_out[base + tid] = status;
+    if (steps_out) steps_out[base + tid] = steps;
+  }
+  if (flags) {
+    unsigned bits = __reduce_or_sync(0xffffffffu, (live && status) ? (1u << status) : 0u);
+    if ((tid & 31) == 0 && bits) atomicOr(flags, (int)bits);
+  }
+  __syncthreads();
+  {
+    float* dstl = evals + base * N;
+    for (int g = tid; g < count * N; g += kSmallThreads) dstl[g] = ltile[(g / N) * Lay::LSTRIDE + g % N];
+    if constexpr (VECS) {
+      float* dst = evecs + base * NN;
+      const int total = count * NN;
+      if ((NN % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        float4* dst4 = reinterpret_cast<float4*>(dst);
+        for (int g4 = tid; g4 < total / 4; g4 += kSmallThreads) {
+          int g = 4 * g4;
+          const float* s = tile + (g / NN) * Lay::STRIDE + (g % NN);
+          dst4[g4] = make_float4(s[0], s[1], s[2], s[3]);
+        }
+      } else {
+        for (int g = tid; g < total; g += kSmallThreads) dst[g] = tile[(g / NN) * Lay::STRIDE + (g % NN)];
+      }
+    }
+  }
+}
+
+}  // namespace bed

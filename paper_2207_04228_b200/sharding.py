@@ -1,0 +1,87 @@
+"""Host-side batch sharding across GPUs (north-star subsystem 5).
+
+The reference solves one batch in one process (its only coupling between
+matrices is the batch-wide deflation gate, _kernels.py:303-318, which the
+device path replaces with per-matrix gating).  With per-matrix gating every
+matrix is independent, so a batch shards into contiguous slices, one per GPU
+(one process per GPU, ``torch.distributed``), with no collective on the hot
+path.  Results are bit-identical for any number of shards.  A gather of the
+outputs (NCCL all-gather over NVLink) is offered only for callers that need
+the whole batch on every rank.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .core import SolverConfig
+
+__all__ = ["shard_bounds", "shard_sizes", "solve_shard", "gather_shards"]
+
+
+def shard_sizes(batch: int, world: int) -> list[int]:
+    """Sizes of the contiguous slices: ceil(batch / world) each, the last
+    ones shorter (possibly empty)."""
+    if batch < 0 or world < 1:
+        raise ValueError("batch must be >= 0 and world >= 1")
+    per = -(-batch // world) if batch else 0
+    return [max(0, min(per, batch - r * per)) for r in range(world)]
+
+
+def shard_bounds(batch: int, world: int, rank: int) -> tuple[int, int]:
+    """[start, stop) of rank's slice."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    per = -(-batch // world) if batch else 0
+    start = min(batch, rank * per)
+    return start, min(batch, start + per)
+
+
+def solve_shard(a: torch.Tensor, cfg: SolverConfig | None = None, *, world: int | None = None,
+                rank: int | None = None, presharded: bool = False,
+                solve_fn: Callable | None = None):
+    """Solve this rank's slice.
+
+    ``a`` is either the full batch (every rank holds it; the rank slices its
+    part) or, with ``presharded=True``, already this rank's slice.  Returns
+    ``(start, stop, result)`` with ``result`` the ``EigenResult`` of the slice.
+    ``solve_fn`` defaults to the device :func:`batched_eig`; tests inject a
+    CPU solver to exercise the host logic without a GPU.
+    """
+    if solve_fn is None:
+        from .solver import batched_eig as solve_fn  # noqa: N813
+    world = dist.get_world_size() if world is None else world
+    rank = dist.get_rank() if rank is None else rank
+    if presharded:
+        sizes = shard_sizes_global(a.shape[0], world)
+        start = sum(sizes[:rank])
+        stop = start + a.shape[0]
+        local = a
+    else:
+        start, stop = shard_bounds(a.shape[0], world, rank)
+        local = a[start:stop]
+    if stop <= start:
+        return start, stop, None
+    return start, stop, solve_fn(local, cfg)
+
+
+def shard_sizes_global(local_batch: int, world: int) -> list[int]:
+    """Slice sizes when every rank holds ``local_batch`` matrices (weak scaling)."""
+    return [local_batch] * world
+
+
+def gather_shards(local: torch.Tensor, batch: int, group=None) -> torch.Tensor:
+    """All-gather rank slices (as cut by :func:`shard_bounds`) into the full
+    batch on every rank.  Uneven tails are padded for the collective and
+    trimmed after."""
+    world = dist.get_world_size(group)
+    sizes = shard_sizes(batch, world)
+    per = max(sizes) if sizes else 0
+    pad = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    out = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(out, pad, group=group)
+    return torch.cat([o[:s] for o, s in zip(out, sizes)], dim=0)

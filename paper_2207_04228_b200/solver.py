@@ -1,0 +1,187 @@
+"""The batched eigendecomposition API on the B200 kernels.
+
+``batched_eig`` keeps the reference facade (``batchedeig.solver.batched_eig``,
+/root/reference/pkg/src/batchedeig/solver.py:79-112): same arguments, same
+result type, same exceptions, same ordering and sign convention.  It runs
+the sm_100a kernels behind ``include/bed200.h`` -- there is no CPU path.
+
+``BatchedEigFn`` is the differentiable form (a ``torch.autograd.Function``)
+whose backward is the paper's Taylor-polynomial gradient (PAPER.md:668,
+:700), which the reference package does not have (pkg/README.md:116-117).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from .core import (
+    BatchedSymmetric,
+    EigenResult,
+    NoConvergence,
+    NonFinite,
+    NonSymmetric,
+    ShapeMismatch,
+    SolveDiagnostics,
+    SolverConfig,
+)
+
+__all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into",
+           "TAYLOR_DEGREE"]
+
+TAYLOR_DEGREE = 9
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_cuda_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be float32, got {t.dtype}")
+    return t.contiguous()
+
+
+def forward_into(A: torch.Tensor, cfg: SolverConfig, evals: torch.Tensor,
+                 evecs: torch.Tensor | None, status: torch.Tensor | None = None,
+                 steps: torch.Tensor | None = None, flags: torch.Tensor | None = None) -> None:
+    """Launch the forward on preallocated device tensors, stream-ordered,
+    without any host synchronisation (the C ABI call ``bed_forward_f32``)."""
+    b, n, _ = A.shape
+    ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    _native.forward_f32(A.data_ptr(), b, n, evals.data_ptr(),
+                        ptr(evecs) if cfg.compute_vectors else None,
+                        ptr(status), ptr(steps), ptr(flags),
+                        _native.make_config(cfg, n), _stream_handle(A.device))
+
+
+def _raise_for_status(A: torch.Tensor, status: torch.Tensor, flags: int, cfg: SolverConfig) -> None:
+    """Map per-matrix status codes onto the reference exceptions.
+
+    Order follows the reference: validate (finiteness over the whole batch
+    first, core.py:297-300, then symmetry, :301-308) before convergence
+    (qr.py:606-609, only when strict).
+    """
+    if flags == 0:
+        return
+    st = status.cpu()
+    if flags & (1 << _native.STATUS_NON_FINITE):
+        k = int(torch.nonzero(st == _native.STATUS_NON_FINITE)[0, 0])
+        bad = torch.nonzero(~torch.isfinite(A[k].detach().cpu()))[0]
+        raise NonFinite(k, (int(bad[0]), int(bad[1])))
+    if flags & (1 << _native.STATUS_NON_SYMMETRIC):
+        k = int(torch.nonzero(st == _native.STATUS_NON_SYMMETRIC)[0, 0])
+        a = A[k].detach().double().cpu()
+        raise NonSymmetric(k, float((a - a.T).abs().max()))
+    if cfg.strict_convergence and flags & (1 << _native.STATUS_NO_CONVERGENCE):
+        idx = torch.nonzero(st == _native.STATUS_NO_CONVERGENCE)[:, 0].tolist()
+        raise NoConvergence(idx, float("nan"))
+
+
+def _solve_device(A: torch.Tensor, cfg: SolverConfig, check: bool = True):
+    A = _check_cuda_f32(A, "A")
+    b, n, _ = A.shape
+    dev = A.device
+    evals = torch.empty((b, n), device=dev, dtype=torch.float32)
+    evecs = torch.empty((b, n, n), device=dev, dtype=torch.float32) if cfg.compute_vectors else None
+    status = torch.empty((b,), device=dev, dtype=torch.int32)
+    steps = torch.empty((b,), device=dev, dtype=torch.int32)
+    flags = torch.empty((1,), device=dev, dtype=torch.int32)
+    with torch.cuda.device(dev):
+        forward_into(A, cfg, evals, evecs, status, steps, flags)
+    if check:
+        _raise_for_status(A, status, int(flags.item()), cfg)
+    return evals, evecs, status, steps
+
+
+def _diagnostics(steps) -> SolveDiagnostics:
+    k = int(steps.max()) if steps.numel() else 0
+    return SolveDiagnostics(double_steps=k, reductions=-1.0, reduction_events=-1,
+                            rotation_count=-1, converged_steps=steps)
+
+
+def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
+    """Full eigendecomposition of a batch of symmetric matrices (solver.py:79-112).
+
+    ``a``: a ``BatchedSymmetric``, a (batch, n, n) numpy array, or a CUDA
+    float32 tensor, 1 <= n <= 64.  Pipeline (all on the GPU, FP32): validate
+    and symmetrise, Householder tridiagonalisation, double-shift QR with
+    per-matrix deflation, eigenvectors accumulated in place, stable sort and
+    sign normalisation.  Host (numpy) inputs are copied through page-locked
+    memory and the results returned as float64 numpy arrays, like the
+    reference; tensor inputs stay on their device.  Raises NonFinite,
+    NonSymmetric and (strict) NoConvergence like the reference.
+    """
+    cfg = cfg or SolverConfig()
+    data = a.data if isinstance(a, BatchedSymmetric) else a
+    if isinstance(data, torch.Tensor):
+        if data.ndim != 3 or data.shape[1] != data.shape[2] or data.shape[0] < 1:
+            raise ShapeMismatch(f"expected (batch, n, n) tensor, got {tuple(data.shape)}")
+        evals, evecs, status, steps = _solve_device(data, cfg)
+        return EigenResult(evals, evecs, _diagnostics(steps))
+    arr = np.asarray(data)
+    if arr.ndim != 3 or arr.shape[1] != arr.shape[2] or arr.shape[0] < 1:
+        raise ShapeMismatch(f"expected (batch, n, n) array, got {arr.shape}")
+    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).pin_memory()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    A = host.to(dev, non_blocking=True)
+    evals, evecs, status, steps = _solve_device(A, cfg)
+    out_l = evals.to("cpu", non_blocking=True)
+    out_v = evecs.to("cpu", non_blocking=True) if evecs is not None else None
+    torch.cuda.current_stream(dev).synchronize()
+    return EigenResult(out_l.numpy().astype(np.float64),
+                       None if out_v is None else out_v.numpy().astype(np.float64),
+                       _diagnostics(steps.cpu().numpy()))
+
+
+def taylor_backward(V: torch.Tensor, evals: torch.Tensor, g_v: torch.Tensor | None,
+                    g_evals: torch.Tensor | None, degree: int = TAYLOR_DEGREE) -> torch.Tensor:
+    """gA = sym(V (F o (V^T gV) + diag(gL)) V^T) with the Taylor-K F (C ABI
+    ``bed_backward_f32``).  Missing cotangents are zero."""
+    V = _check_cuda_f32(V, "V")
+    evals = _check_cuda_f32(evals, "evals")
+    b, n, _ = V.shape
+    gv = None if g_v is None else _check_cuda_f32(g_v, "g_v")
+    gl = None if g_evals is None else _check_cuda_f32(g_evals, "g_evals")
+    gA = torch.empty_like(V)
+    with torch.cuda.device(V.device):
+        _native.backward_f32(V.data_ptr(), evals.data_ptr(),
+                             None if gv is None else gv.data_ptr(),
+                             None if gl is None else gl.data_ptr(),
+                             gA.data_ptr(), b, n, int(degree), _stream_handle(V.device))
+    return gA
+
+
+class BatchedEigFn(torch.autograd.Function):
+    """Differentiable batched ED: forward = ``bed_forward_f32``, backward =
+    the Taylor-polynomial gradient ``bed_backward_f32`` (degree 9 by default).
+
+    ``check=False`` skips the host read of the status word, keeping the
+    forward free of device-to-host synchronisation (for training loops).
+    """
+
+    @staticmethod
+    def forward(ctx, A, cfg: SolverConfig | None = None, degree: int = TAYLOR_DEGREE,
+                check: bool = True):
+        cfg = cfg or SolverConfig()
+        if not cfg.compute_vectors:
+            raise ValueError("the differentiable ED needs compute_vectors=True")
+        evals, evecs, _, _ = _solve_device(A.detach(), cfg, check=check)
+        ctx.save_for_backward(evals, evecs)
+        ctx.degree = degree
+        return evals, evecs
+
+    @staticmethod
+    def backward(ctx, g_evals, g_evecs):
+        evals, evecs = ctx.saved_tensors
+        gA = taylor_backward(evecs, evals, g_evecs, g_evals, ctx.degree)
+        return gA, None, None, None
+
+
+def eigh(A: torch.Tensor, cfg: SolverConfig | None = None, degree: int = TAYLOR_DEGREE,
+         check: bool = True):
+    """(eigenvalues, eigenvectors) of a CUDA float32 batch, differentiable."""
+    return BatchedEigFn.apply(A, cfg, degree, check)

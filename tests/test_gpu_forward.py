@@ -1,0 +1,206 @@
+"""GPU parity tests of the forward ED against the reference (golden fixtures)
+and the C oracle.  Every solve goes through the C ABI (libbed200.so)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import parity as P
+
+pytestmark = pytest.mark.gpu
+
+VERIFY = dict(deflation_tol=3e-12)
+
+
+@pytest.fixture(scope="module")
+def bed():
+    import paper_2207_04228_b200 as bed
+
+    return bed
+
+
+def _cell_names():
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "cells.npz"))
+    return sorted({k.split("/")[0] for k in z.files if k.endswith("/a")})
+
+
+def _solve(bed, a32, **kw):
+    cfg = bed.SolverConfig(max_double_steps=4 * a32.shape[1], **kw)
+    r = bed.batched_eig(torch.from_numpy(a32).cuda(), cfg)
+    v = None if r.eigenvectors is None else r.eigenvectors.cpu().numpy()
+    return r.eigenvalues.cpu().numpy(), v, r
+
+
+@pytest.mark.parametrize("name", _cell_names())
+@pytest.mark.parametrize("tol", [3e-12, 1e-5])
+def test_golden_cells(bed, cells, name, tol):
+    a32 = cells[f"{name}/a"]
+    a = a32.astype(np.float64)
+    ref_l = cells[f"{name}/verify/evals"]
+    ref_v = cells[f"{name}/verify/evecs"]
+    lam, vec, _ = _solve(bed, a32, deflation_tol=tol)
+    assert np.all(P.eig_err(lam, ref_l) <= P.EIG_TOL), P.eig_err(lam, ref_l).max()
+    assert np.all(P.recon_err(a, lam, vec) <= P.RECON_TOL), P.recon_err(a, lam, vec).max()
+    assert np.all(P.orth_err(vec) <= P.ORTH_TOL), P.orth_err(vec).max()
+    if not name.startswith("edge"):
+        assert np.all(P.vector_err(vec, ref_v, ref_l) <= 1.0), P.vector_err(vec, ref_v, ref_l).max()
+    # descending order, sign convention
+    assert np.all(np.diff(lam, axis=1) <= 0)
+    lead = np.take_along_axis(vec, np.argmax(np.abs(vec), axis=1)[:, None, :], axis=1)
+    assert lead.min() >= 0.0
+
+
+def test_known_answers(bed, known):
+    lam, vec, _ = _solve(bed, known["diag123/a"].astype(np.float32))
+    np.testing.assert_array_equal(lam, known["diag123/evals"])
+    np.testing.assert_array_equal(vec, known["diag123/evecs"])
+    lam, vec, _ = _solve(bed, known["classic2x2/a"].astype(np.float32))
+    np.testing.assert_allclose(lam, known["classic2x2/evals"], rtol=2e-7)
+    np.testing.assert_allclose(vec, known["classic2x2/evecs"], rtol=2e-7)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 13, 16, 20, 24, 31, 32, 33, 40, 48, 57, 64])
+def test_every_size_against_oracle(bed, n):
+    b = 37 if n > 8 else 301  # ragged: not a multiple of any CTA tile
+    a = oracle.gen_spd(b, n, 1000 + n).astype(np.float32)
+    lam, vec, r = _solve(bed, a, **VERIFY)
+    o = oracle.forward(a.astype(np.float64))
+    assert np.all(P.eig_err(lam, o.eigenvalues) <= P.EIG_TOL)
+    assert np.all(P.recon_err(a.astype(np.float64), lam, vec) <= P.RECON_TOL)
+    assert np.all(P.orth_err(vec) <= P.ORTH_TOL)
+    assert np.all(P.vector_err(vec, o.eigenvectors, o.eigenvalues) <= 1.0)
+    steps = r.diagnostics.converged_steps.cpu().numpy()
+    assert steps.max() <= 4 * n
+
+
+@pytest.mark.parametrize("n", [4, 16, 32, 64])
+def test_values_only_matches_full_bitwise(bed, n):
+    a = oracle.gen_spd(64, n, 7).astype(np.float32)
+    full, _, _ = _solve(bed, a, **VERIFY)
+    vals, vec, _ = _solve(bed, a, compute_vectors=False, **VERIFY)
+    assert vec is None
+    np.testing.assert_array_equal(vals, full)
+
+
+@pytest.mark.parametrize("n", [4, 16, 48])
+def test_sort_orders(bed, n):
+    a = oracle.gen_spd(40, n, 3).astype(np.float32)
+    desc, vd, _ = _solve(bed, a, **VERIFY)
+    asc, va, _ = _solve(bed, a, sort="ascending", **VERIFY)
+    none, vn, _ = _solve(bed, a, sort="none", **VERIFY)
+    np.testing.assert_array_equal(asc, desc[:, ::-1])
+    np.testing.assert_array_equal(va, vd[:, :, ::-1])
+    np.testing.assert_array_equal(np.sort(none, axis=1), np.sort(desc, axis=1))
+
+
+@pytest.mark.parametrize("n", [4, 16, 64])
+def test_partition_independence_bitwise(bed, n):
+    """Per-matrix deflation: a matrix's result does not depend on its batch."""
+    a = oracle.gen_spd(96, n, 11).astype(np.float32)
+    full, vf, _ = _solve(bed, a, **VERIFY)
+    for lo, hi in ((0, 1), (5, 40), (40, 96)):
+        part, vp, _ = _solve(bed, np.ascontiguousarray(a[lo:hi]), **VERIFY)
+        np.testing.assert_array_equal(part, full[lo:hi])
+        np.testing.assert_array_equal(vp, vf[lo:hi])
+
+
+def test_scale_equivariance(bed):
+    a = oracle.gen_spd(16, 8, 4).astype(np.float32)
+    base, vb, _ = _solve(bed, a, **VERIFY)
+    for c in (2.0 ** -10, 8.0, 2.0 ** 10):  # exact powers of two: identical problems
+        s, vs, _ = _solve(bed, (a * np.float32(c)).astype(np.float32), **VERIFY)
+        np.testing.assert_array_equal(s, base * np.float32(c))
+        np.testing.assert_array_equal(vs, vb)
+
+
+def test_errors(bed):
+    a = np.stack([np.eye(4, dtype=np.float32)] * 3)
+    bad = a.copy()
+    bad[1, 2, 3] = np.nan
+    with pytest.raises(bed.NonFinite) as e:
+        bed.batched_eig(torch.from_numpy(bad).cuda())
+    assert e.value.batch_index == 1 and e.value.position == (2, 3)
+    asym = a.copy()
+    asym[2, 0, 1] = 1.0
+    with pytest.raises(bed.NonSymmetric) as e:
+        bed.batched_eig(torch.from_numpy(asym).cuda())
+    assert e.value.batch_index == 2
+    hard = oracle.gen_spd(64, 16, 5).astype(np.float32)
+    with pytest.raises(bed.NoConvergence):
+        bed.batched_eig(torch.from_numpy(hard).cuda(),
+                        bed.SolverConfig(deflation_tol=3e-12, max_double_steps=1))
+    # fixed schedule: no error, diagonal locked
+    r = bed.batched_eig(torch.from_numpy(hard).cuda(),
+                        bed.SolverConfig(deflation_tol=3e-12, max_double_steps=1,
+                                         strict_convergence=False))
+    assert r.eigenvalues.shape == (64, 16)
+
+
+def test_numpy_host_path_and_batched_symmetric(bed, cells):
+    a32 = cells["c1_n4_b512/a"]
+    r = bed.batched_eig(bed.BatchedSymmetric(a32.astype(np.float64)),
+                        bed.SolverConfig(**VERIFY, max_double_steps=16))
+    assert isinstance(r.eigenvalues, np.ndarray) and r.eigenvalues.dtype == np.float64
+    assert np.all(P.eig_err(r.eigenvalues, cells["c1_n4_b512/verify/evals"]) <= P.EIG_TOL)
+
+
+def test_c_abi_host_entry(bed):
+    """bed_forward_host_f32 on plain numpy buffers -- the call a non-torch FFI makes."""
+    from paper_2207_04228_b200 import _native
+
+    for n, b in ((4, 5000), (24, 300)):
+        a = oracle.gen_spd(b, n, 21).astype(np.float32)
+        lam = np.zeros((b, n), np.float32)
+        vec = np.zeros((b, n, n), np.float32)
+        st = np.zeros(b, np.int32)
+        k = np.zeros(b, np.int32)
+        cfg = _native.make_config(bed.SolverConfig(max_double_steps=4 * n, **VERIFY), n)
+        _native.forward_host_f32(a.ctypes.data, b, n, lam.ctypes.data, vec.ctypes.data,
+                                 st.ctypes.data, k.ctypes.data, cfg, 0)
+        dev, vdev, _ = _solve(bed, a, **VERIFY)
+        np.testing.assert_array_equal(lam, dev)
+        np.testing.assert_array_equal(vec, vdev)
+        assert st.max() == 0 and k.min() >= 1
+
+
+def test_c_abi_rejects_bad_arguments(bed):
+    from paper_2207_04228_b200 import _native
+
+    L = _native.lib()
+    cfg = _native.make_config(bed.SolverConfig(), 4)
+    x = torch.zeros((2, 4, 4), device="cuda")
+    y = torch.zeros((2, 4), device="cuda")
+    assert L.bed_forward_f32(x.data_ptr(), 2, 65, y.data_ptr(), x.data_ptr(), None, None, None,
+                             ctypes.byref(cfg), None) == 1
+    assert L.bed_forward_f32(x.data_ptr(), 2, 4, None, x.data_ptr(), None, None, None,
+                             ctypes.byref(cfg), None) == 1
+    assert L.bed_forward_f32(x.data_ptr() + 2, 2, 4, y.data_ptr(), x.data_ptr(), None, None, None,
+                             ctypes.byref(cfg), None) == 2
+    assert L.bed_forward_f32(x.data_ptr(), 0, 4, y.data_ptr(), x.data_ptr(), None, None, None,
+                             ctypes.byref(cfg), None) == 0
+
+
+@pytest.mark.parametrize("n,b", [(4, 1 << 20), (16, 65536), (64, 2048)])
+def test_large_batch_properties(bed, n, b):
+    """Full-size batches: invariants on every matrix, oracle on a sample."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn((b, n, n), device="cuda", generator=g)
+    a = x @ x.transpose(1, 2) / n + 1e-3 * torch.eye(n, device="cuda")
+    a = 0.5 * (a + a.transpose(1, 2))
+    r = bed.batched_eig(a, bed.SolverConfig(**VERIFY, max_double_steps=4 * n))
+    lam, v = r.eigenvalues, r.eigenvectors
+    ad = a.double()
+    rec = torch.linalg.matrix_norm(ad @ v.double() - v.double() * lam.double()[:, None, :])
+    rec = rec / torch.linalg.matrix_norm(ad)
+    orth = torch.linalg.matrix_norm(v.double().transpose(1, 2) @ v.double() - torch.eye(n, device="cuda", dtype=torch.float64)) / n
+    assert float(rec.max()) <= P.RECON_TOL
+    assert float(orth.max()) <= P.ORTH_TOL
+    assert bool((lam[:, 1:] <= lam[:, :-1]).all())
+    idx = torch.randperm(b, generator=torch.Generator().manual_seed(0))[:64]
+    o = oracle.forward(a[idx.cuda()].double().cpu().numpy())
+    assert np.all(P.eig_err(lam[idx.cuda()].cpu().numpy(), o.eigenvalues) <= P.EIG_TOL)
