@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark: batched symmetric ED (arXiv 2207.04228) on B200.
+
+Headline (BASELINE.json configs[1]): 4x4 ED forward, 4,194,304 matrices per
+GPU (weak scaling across ranks), matrices/second over the whole job.  A step
+is one forward pass over the resident batch (one kernel launch); inputs are
+generated on the device before timing and the 576 MB working set exceeds the
+126 MB L2, so no flush is needed between steps.
+
+Run:  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+Prints ONE JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched ED matrices/sec (fwd, fwd+bwd) vs n, batch; frac of HBM/FP32 roofline"
+UNIT = "matrices/s"
+HEADLINE = dict(name="c2_fwd_n4", n=4, batch=4194304, mode="fwd")
+# accuracy profile of every timed run: the reference verify profile
+# (bench.py:40, bench.py:227-228): tol 3e-12 (the kernels floor it at the FP32
+# limit 2^-22) and a 4n double-step budget -- the profile whose results pass
+# the parity gates (tests/parity.py).
+TOL = 3e-12
+FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9  # FFMA, nominal at max clock
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]) * 1e9, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6.65e12, "fallback (B200_PROFILING.md)"
+
+
+def work_per_matrix(n: int, mode: str):
+    """algorithmic flops and bytes per matrix."""
+    f_fwd = (8.0 / 3.0) * n ** 3 + (6 * n + 24) * n * (n - 1)
+    b_fwd = 4 * (2 * n * n + n)
+    if mode == "fwd":
+        return f_fwd, b_fwd
+    f_bwd = 6 * n ** 3 + 22 * n * n
+    b_bwd = 4 * (3 * n * n + 2 * n)
+    return f_fwd + f_bwd, b_fwd + b_bwd
+
+
+def roofline(n, mode, batch, seconds, hbm_peak):
+    flops, nbytes = work_per_matrix(n, mode)
+    t_hbm = batch * nbytes / hbm_peak
+    t_f32 = batch * flops / FP32_PEAK_NOMINAL
+    bound = "hbm" if t_hbm >= t_f32 else "fp32"
+    return bound, max(t_hbm, t_f32) / seconds, flops * batch, nbytes * batch
+
+
+class ClockSampler:
+    """NVML poller (5 ms) of SM clock and throttle reasons during a region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            pass
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_inputs(torch, n, batch, mode, seed, dev):
+    from paper_2207_04228_b200.datagen import covariance_device, gen_spd_device
+
+    if mode == "fwdbwd" and n <= 16:
+        a = covariance_device(batch, n, 4 * n, seed, device=dev)
+    else:
+        a = gen_spd_device(batch, n, seed, device=dev)
+    return a
+
+
+class Step:
+    """One step of a workload on preallocated device buffers."""
+
+    def __init__(self, torch, bed, n, batch, mode, dev, seed):
+        self.torch, self.bed, self.n, self.batch, self.mode = torch, bed, n, batch, mode
+        self.a = make_inputs(torch, n, batch, mode, seed, dev)
+        self.cfg = bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n)
+        self.lam = torch.empty((batch, n), device=dev)
+        self.vec = torch.empty((batch, n, n), device=dev)
+        self.status = torch.empty((batch,), device=dev, dtype=torch.int32)
+        self.steps = torch.empty((batch,), device=dev, dtype=torch.int32)
+        if mode == "fwdbwd":
+            g = torch.Generator(device=dev).manual_seed(seed + 1)
+            self.gv = torch.randn((batch, n, n), device=dev, generator=g)
+            self.gl = torch.randn((batch, n), device=dev, generator=g)
+        self.launches = 1 if mode == "fwd" else 2
+
+    def __call__(self):
+        self.bed.forward_into(self.a, self.cfg, self.lam, self.vec, self.status, self.steps)
+        if self.mode == "fwdbwd":
+            self.ga = self.bed.taylor_backward(self.vec, self.lam, self.gv, self.gl)
+
+
+def time_steps(torch, step, k, w, dist=None):
+    for _ in range(w):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) * 1e-3
+    if dist is not None:
+        t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        sec = float(t.item())
+    return sec
+
+
+def cpu_oracle_rate(n, sample, threads, mode="fwd"):
+    """Matrices/s of the reference algorithm's C restatement (oracle/) on
+    host cores: per-matrix gating, same tolerance/budget as the GPU run."""
+    import oracle
+
+    a = oracle.gen_spd(sample, n, 12345)
+    t0 = time.perf_counter()
+    r = oracle.forward(a, deflation_tol=TOL, max_double_steps=4 * n, gate=oracle.GATE_MATRIX,
+                       threads=threads, chunk=max(64, sample // (8 * threads)))
+    t1 = time.perf_counter()
+    sec = t1 - t0
+    if mode == "fwdbwd":
+        rng = np.random.default_rng(1)
+        gv = rng.standard_normal((sample, n, n))
+        t0 = time.perf_counter()
+        oracle.taylor_backward(r.eigenvectors, r.eigenvalues, gv, None)
+        sec += time.perf_counter() - t0
+    return sample / sec, sec
+
+
+def calibrated_sample(n, threads, target_s, cap):
+    rate, _ = cpu_oracle_rate(n, 2048 if n <= 16 else 256, threads)
+    return int(max(256, min(cap, rate * target_s)))
+
+
+def e2e_host(torch, bed, n, batch, steps, dev_index):
+    """Same metric through the C ABI host-buffer entry bed_forward_host_f32
+    (the reference-facing call on numpy-side buffers): per step the H2D copy
+    of A from page-locked memory, the solve, and the D2H copy of eigenvalues,
+    eigenvectors and per-matrix status, all inside the timed region."""
+    from paper_2207_04228_b200 import _native
+
+    a = bed.datagen.gen_spd_device(batch, n, 7, device=f"cuda:{dev_index}").cpu().pin_memory()
+    lam = torch.empty((batch, n), dtype=torch.float32).pin_memory()
+    vec = torch.empty((batch, n, n), dtype=torch.float32).pin_memory()
+    st = torch.empty((batch,), dtype=torch.int32).pin_memory()
+    cfg = _native.make_config(bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n), n)
+    call = lambda: _native.forward_host_f32(a.data_ptr(), batch, n, lam.data_ptr(),  # noqa: E731
+                                            vec.data_ptr(), st.data_ptr(), None, cfg, dev_index)
+    call()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    assert int(st.max()) == 0, "e2e solve reported a nonzero status"
+    sec = statistics.median(times)
+    return {"value": batch / sec, "unit": UNIT, "h2d_bytes_per_step": 4 * batch * n * n,
+            "d2h_bytes_per_step": 4 * batch * (n * n + n) + 4 * batch,
+            "path": "C ABI bed_forward_host_f32, page-locked host buffers, median of "
+                    f"{steps} calls (chunked 3-stream copy/compute overlap)"}
+
+
+def load_traffic(name):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(name, {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2207_04228_b200 as bed
+    import paper_2207_04228_b200.datagen  # noqa: F401
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    hbm_peak, peak_src = peaks()
+    n, batch = HEADLINE["n"], HEADLINE["batch"]
+    step = Step(torch, bed, n, batch, "fwd", dev, seed=100 + rank)
+    with ClockSampler(local) as clk:
+        sec = time_steps(torch, step, args.steps, args.warmup, pg)
+    per_step = sec / args.steps
+    value = world * batch / per_step
+    bound, frac, flops, nbytes = roofline(n, "fwd", batch, per_step, hbm_peak)
+    achieved = nbytes / per_step / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: Q diag(lam) Q^T, lam log-uniform over 3 decades (reference gen_spd "
+                "distribution), generated on device",
+        "config": {"workload": "c2: 4x4 ED forward, 4194304 matrices per GPU", "n": n,
+                   "batch_per_gpu": batch, "global_batch": world * batch,
+                   "deflation_tol": TOL, "effective_deflation_tol": 2.0 ** -22,
+                   "max_double_steps": 4 * n, "gating": "per-matrix",
+                   "l2": "no flush: 576 MB working set per step > 126 MB L2",
+                   "parallelism": f"batch sharded, {world} rank(s), no collective"},
+        "gpu_launches": args.steps * step.launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak / 1e9,
+                     "unit": "GB/s", "frac": achieved / (hbm_peak / 1e9),
+                     "traffic": load_traffic("bed_small_kernel<4,true>"),
+                     "kernel": "bed_small_kernel<4, true>", "peak_source": peak_src,
+                     "bytes_per_matrix": work_per_matrix(n, "fwd")[1],
+                     "fp32_frac_nominal": flops / per_step / FP32_PEAK_NOMINAL},
+        "clocks": clk.summary(),
+    }
+    mean_steps = float(step.steps.float().mean())
+    line["config"]["mean_double_steps"] = mean_steps
+    line["config"]["max_double_steps_used"] = int(step.steps.max())
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line["e2e"] = e2e_host(torch, bed, n, batch, max(3, min(args.steps, 10)), local)
+        if not args.quick:
+            line["other_configs"] = other_configs(torch, bed, dev, hbm_peak)
+        threads = os.cpu_count() or 1
+        sample = calibrated_sample(n, threads, 3.0, 1 << 20)
+        rate, secs = cpu_oracle_rate(n, sample, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{sample} 4x4 matrices (same distribution), oracle/ "
+                                          "C restatement of the reference solver, per-matrix gate, "
+                                          f"tol {TOL:g}, budget 16, {threads} threads, {secs:.2f} s"}
+        try:
+            sub = step.a[:16384].contiguous()
+            torch.linalg.eigh(sub)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            torch.linalg.eigh(sub)
+            torch.cuda.synchronize()
+            te = time.perf_counter() - t0
+            line["torch_eigh_baseline"] = {"value": sub.shape[0] / te, "unit": UNIT,
+                                           "batch": sub.shape[0], "what": "torch.linalg.eigh fp32 on 1 B200"}
+        except Exception as exc:  # noqa: BLE001
+            line["torch_eigh_baseline"] = {"unavailable": str(exc)[:120]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def other_configs(torch, bed, dev, hbm_peak):
+    """C1/C3 (b=512, launch-bound), C4 (n=16 fwd+bwd), C5 (n=64 fwd+bwd),
+    and the n sweep at large batch -- reported beside the headline."""
+    rows = []
+    cases = [(4, 512, "fwd"), (8, 512, "fwd"), (16, 512, "fwd"), (24, 512, "fwd"), (32, 512, "fwd"),
+             (8, 1 << 20, "fwd"), (16, 1 << 18, "fwd"), (24, 1 << 17, "fwd"), (32, 1 << 16, "fwd"),
+             (64, 8192, "fwd"), (16, 65536, "fwdbwd"), (64, 8192, "fwdbwd")]
+    for n, b, mode in cases:
+        st = Step(torch, bed, n, b, mode, dev, seed=n)
+        reps = 50 if b <= 4096 else 10
+        sec = time_steps(torch, st, reps, 3) / reps
+        bound, frac, _, _ = roofline(n, mode, b, sec, hbm_peak)
+        rows.append({"n": n, "batch": b, "mode": mode, "ms": sec * 1e3, "value": b / sec,
+                     "roofline_bound": bound, "roofline_frac": frac,
+                     "mean_double_steps": float(st.steps.float().mean())})
+    return rows
+
+
+def run_reference(args):
+    """The reference algorithm on the host cores (oracle/ C restatement:
+    the reference is numba Python that cannot travel to the GPU box), same
+    config, metric and unit; each step a bounded sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = HEADLINE["n"]
+    threads = os.cpu_count() or 1
+    budget = 60.0 / max(1, args.steps + args.warmup)
+    sample = calibrated_sample(n, threads, budget, HEADLINE["batch"])
+    for _ in range(args.warmup):
+        cpu_oracle_rate(n, sample, threads)
+    secs = [cpu_oracle_rate(n, sample, threads)[1] for _ in range(args.steps)]
+    sec = statistics.median(secs)
+    value = sample / sec
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic: reference gen_spd restatement (oracle.gen_spd)",
+        "config": {"workload": "c2: 4x4 ED forward (bounded host sample per step)", "n": n,
+                   "batch_per_step": sample, "deflation_tol": TOL, "max_double_steps": 4 * n,
+                   "gating": "per-matrix"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} matrices per step, oracle/bed_oracle.c (float64 "
+                                   f"restatement of batchedeig.batched_eig), {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--quick", action="store_true", help="skip the other_configs sweep")
+    args = p.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

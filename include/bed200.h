@@ -45,7 +45,7 @@ extern "C" {
 /* Return codes of every entry point. */
 #define BED_SUCCESS 0
 #define BED_ERR_INVALID_ARGUMENT 1 /* null pointer, n out of [1, 64], batch < 0, bad enum */
-#define BED_ERR_MISALIGNED 2       /* device pointer not 16-byte aligned */
+#define BED_ERR_MISALIGNED 2       /* pointer not aligned to its 4-byte element size */
 #define BED_ERR_CUDA 3             /* launch / runtime failure (see bed_last_cuda_error) */
 #define BED_ERR_NO_DEVICE 4        /* no sm_100 device visible */
 
@@ -63,7 +63,8 @@ extern "C" {
 
 /* SolverConfig (core.py:226-279) as the kernels see it. */
 typedef struct bed_config {
-  float deflation_tol;      /* absolute, on the power-of-two equilibrated band (qr.py:512-515) */
+  float deflation_tol;      /* absolute, on the power-of-two equilibrated band (qr.py:512-515);
+                               values below the FP32 floor 2^-22 act as 2^-22 */
   float symmetry_tol;       /* relative asymmetry tolerance (core.py:254) */
   int32_t max_double_steps; /* <= 0 resolves to 2n (core.py:270-271) */
   int32_t sort;             /* BED_SORT_* */

@@ -98,7 +98,7 @@ def _solve_device(A: torch.Tensor, cfg: SolverConfig, check: bool = True):
 
 
 def _diagnostics(steps) -> SolveDiagnostics:
-    k = int(steps.max()) if steps.numel() else 0
+    k = int(steps.max()) if len(steps) else 0
     return SolveDiagnostics(double_steps=k, reductions=-1.0, reduction_events=-1,
                             rotation_count=-1, converged_steps=steps)
 

@@ -1,0 +1,27 @@
+"""One launch of each main kernel configuration, for ncu captures."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2207_04228_b200 as bed  # noqa: E402
+from paper_2207_04228_b200.datagen import covariance_device, gen_spd_device  # noqa: E402
+
+torch.cuda.set_device(0)
+cases = [(4, 1 << 22, False), (8, 1 << 20, False), (16, 65536, True), (32, 65536, False),
+         (64, 8192, True)]
+which = sys.argv[1:] or None
+for n, b, bwd in cases:
+    if which and str(n) not in which:
+        continue
+    a = covariance_device(b, n, 4 * n, 0) if n == 16 else gen_spd_device(b, n, 0)
+    cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n)
+    lam = torch.empty((b, n), device="cuda")
+    vec = torch.empty((b, n, n), device="cuda")
+    bed.forward_into(a, cfg, lam, vec)
+    if bwd:
+        gv = torch.randn_like(vec)
+        gl = torch.randn_like(lam)
+        bed.taylor_backward(vec, lam, gv, gl)
+    torch.cuda.synchronize()
+print("done")
