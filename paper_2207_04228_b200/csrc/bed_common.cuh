@@ -13,6 +13,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <string.h>
+
 #include <type_traits>
 
 #define BED_HD __host__ __device__ __forceinline__
@@ -38,7 +40,9 @@ struct KernelCfg {
 
 BED_HD float rsqrt_approx(float x) {
 #ifdef __CUDA_ARCH__
-  return rsqrtf(x);
+  float y;  // one MUFU.RSQ; inputs here are normal numbers (no denormal fixup)
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 #else
   return 1.0f / sqrtf(x);
 #endif
@@ -55,29 +59,46 @@ BED_HD float rsqrt_nr(float x) {
 
 // Givens rotation annihilating e against dw: R^T (dw, e) = (r, 0) with
 // R = [[c, s], [-s, c]] (tests/helpers.py:14-22 convention, s = -e/r).
+// A zero target gives the identity exactly (_kernels.py:247, :256-258); so
+// does a target below 2^-60 of the equilibrated band (unit scale), which is
+// far below FP32 resolution of any band entry it could couple.  With
+// |e| >= 2^-60 the square sum is a normal number, so no scaled branch is
+// needed (the reference's branch-scaled form, _kernels.py:248-258, guards
+// float64 over/underflow that the equilibrated band cannot reach).
 BED_HD void givens(float dw, float e, float& c, float& s, float& r) {
-  if (e == 0.0f) {
-    c = 1.0f;
-    s = 0.0f;
-    r = dw;
-    return;
-  }
-  float h2 = fmaf(dw, dw, e * e);
-  if (h2 > 1e-30f && h2 < 1e30f) {
-    float ih = rsqrt_nr(h2);
-    c = dw * ih;
-    s = -e * ih;
-    r = h2 * ih;
-  } else {  // branch-scaled form of the reference (_kernels.py:248-258)
-    float am = fmaxf(fabsf(dw), fabsf(e));
-    float iam = 1.0f / am;
-    float t1 = dw * iam, t2 = e * iam;
-    float hh2 = fmaf(t1, t1, t2 * t2);
-    float ih = rsqrt_nr(hh2);
-    c = t1 * ih;
-    s = -t2 * ih;
-    r = am * (hh2 * ih);
-  }
+  const bool live = fabsf(e) >= 0x1p-60f;
+  const float h2 = fmaf(dw, dw, e * e);
+  const float ih = rsqrt_nr(h2);
+  c = live ? dw * ih : 1.0f;
+  s = live ? -e * ih : 0.0f;
+  r = live ? h2 * ih : dw;
+}
+
+// Shift pair only (no rotation), fast math: the shifts steer convergence
+// but every sweep is an exact similarity whatever their rounding, so they
+// need not be correctly rounded.  hi is the root nearer d (applied first,
+// qr.py:67-76); b == 0 gives (a, d) exactly like the reference shortcut.
+BED_HD void wilkinson_shifts(float a, float b, float d, float& lo, float& hi) {
+  const float h = 0.5f * (a - d);
+  const float q = fmaf(h, h, b * b);
+  const float rad = q > 0.0f ? q * rsqrt_approx(q) : 0.0f;
+  const float mid = 0.5f * (a + d);
+  const float nearer = h >= 0.0f ? mid - rad : mid + rad;
+  const float farther = h >= 0.0f ? mid + rad : mid - rad;
+  hi = b == 0.0f ? d : nearer;
+  lo = b == 0.0f ? a : farther;
+}
+
+// Fast reciprocal (one MUFU.RCP): the reflector code only needs a ratio that
+// is used consistently; normalisation happens afterwards with rsqrt_nr.
+BED_HD float rcp_fast(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#else
+  return 1.0f / x;
+#endif
 }
 
 // Eigenvalue pair of [[a, b], [b, d]] plus its diagonalising rotation.
@@ -101,13 +122,33 @@ BED_HD void wilkinson(float a, float b, float d, float& lo, float& hi, float& c,
   hi = (a * s * s + bcs2) + d * c * c;
 }
 
-// 2^ceil(log2(top)) for top > 0 (1 for top == 0), computed exactly.
-BED_HD float pow2_ceil(float top) {
-  if (!(top > 0.0f)) return 1.0f;
-  int ex;
-  float f = frexpf(top, &ex);  // top = f * 2^ex, f in [0.5, 1)
-  if (f == 0.5f) ex -= 1;
-  return ldexpf(1.0f, ex);
+BED_HD float bits_to_float(int b) {
+#ifdef __CUDA_ARCH__
+  return __int_as_float(b);
+#else
+  float f;
+  memcpy(&f, &b, sizeof f);
+  return f;
+#endif
+}
+
+// 2^ceil(log2(top)) for top > 0 (1 for top == 0), computed exactly from the
+// exponent bits; returns the power and its exact inverse.
+BED_HD float pow2_ceil(float top, float* inv = nullptr) {
+  float p = 1.0f, ip = 1.0f;
+  if (top > 0.0f && top <= 0x1p126f) {
+    int ex;
+    const float f = frexpf(top, &ex);  // top = f * 2^ex, f in [0.5, 1)
+    if (f == 0.5f) ex -= 1;
+    ex = ex < -125 ? -125 : ex;
+    p = bits_to_float((ex + 127) << 23);
+    ip = bits_to_float((127 - ex) << 23);
+  } else if (top > 0x1p126f) {
+    p = 0x1p127f;
+    ip = 0x1p-127f;
+  }
+  if (inv) *inv = ip;
+  return p;
 }
 
 // Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).  Used

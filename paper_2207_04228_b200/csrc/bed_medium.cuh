@@ -33,6 +33,8 @@
 
 namespace bed {
 
+constexpr int kFoldBlk = 8;  // fold granularity (positions per static block)
+
 template <int NMAX, int T_, int S_>
 struct MedParams {
   static constexpr int L = NMAX <= 16 ? 16 : (NMAX <= 32 ? 32 : 64);
@@ -193,14 +195,16 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
     const float scale = grp.max(fabsf(x));
     float* urow = st + i * P::SROW;
     if (scale > kZeroTail) {
-      const float xs = x * (1.0f / scale);
+      // reflector of the scaled tail xs = tail/scale (householder.py:97-118):
+      // sigma = sign(xs_0) ||xs||, u0 = xs_0 + sigma, ||u||^2 = 2 sigma u0
+      const float xs = x * rcp_fast(scale);
       const float ss = grp.sum(xs * xs);
-      const float norm = scale * sqrtf(ss);
-      const float pivot = grp.bcast(x, i + 1);
-      const float sigma = pivot >= 0.0f ? norm : -norm;
+      const float pivot = grp.bcast(xs, i + 1);
+      const float nrm = ss * rsqrt_nr(ss);
+      const float sigma = pivot >= 0.0f ? nrm : -nrm;
       const float u0 = pivot + sigma;
-      const float iu = 1.0f / (sqrtf(2.0f * fabsf(sigma)) * sqrtf(fabsf(u0)));
-      const float u = (r == i + 1 ? u0 : x) * iu;  // x = 0 for r <= i
+      const float iu = rsqrt_nr(2.0f * sigma * u0);  // sigma, u0 share a sign
+      const float u = (r == i + 1 ? u0 : xs) * iu;  // xs = 0 for r <= i
       if (r < NMAX) urow[r] = u;
       grp.sync();
       // p = 2 A u, K = u^T p, q = p - K u (zero above row i)
@@ -271,8 +275,8 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
       top = fmaxf(top, fabsf(Dg[c * T + k]));
       if (c + 1 < n) top = fmaxf(top, fabsf(Eg[c * T + k]));
     }
-    bscale = pow2_ceil(top);
-    const float inv = 1.0f / bscale;  // exact: power of two
+    float inv;
+    bscale = pow2_ceil(top, &inv);  // exact powers of two
     for (int c = 0; c < n; ++c) {
       Dg[c * T + k] *= inv;
       if (c + 1 < n) Eg[c * T + k] *= inv;
@@ -280,17 +284,25 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
     while (bm > 2 && fabsf(Eg[(bm - 2) * T + k]) < cfg.eps) --bm;  // initial deflation
   }
 
-  // one explicit shifted sweep of the leading m-block (_sweep_block)
+  // One explicit shifted sweep of the leading m-block (_sweep_block), run by
+  // the band lane of matrix k out of shared memory.  The loads of d[i+2] and
+  // e[i+2] are issued one iteration ahead so only the register recurrence
+  // (dw -> rotation -> dw) is on the critical path.  Rotations past the
+  // active block, up to the next multiple of kFoldBlk, are recorded as the
+  // identity so the fold runs whole static blocks.
   auto sweep = [&](int k, int m, float mu, int slot) {
-    float dw = Dg[k] - mu, g = Eg[k];
-    float c1 = 1.0f, s1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
     float2* rs = rot + (size_t)slot * (NMAX - 1) * T + k;
+    float dw = Dg[k] - mu, g = Eg[k];
+    float ei = g;
+    float dnx = Dg[T + k];
+    float en = m > 2 ? Eg[T + k] : 0.0f;
+    float c1 = 1.0f, s1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
     for (int i = 0; i < m - 1; ++i) {
-      const float ei = Eg[i * T + k];
-      const float dn = Dg[(i + 1) * T + k] - mu;
-      const float en = (i < m - 2) ? Eg[(i + 1) * T + k] : 0.0f;
+      const float dnx2 = i + 2 < m ? Dg[(i + 2) * T + k] : 0.0f;
+      const float en2 = i + 2 < m - 1 ? Eg[(i + 2) * T + k] : 0.0f;
       float c, s, rr;
       givens(dw, ei, c, s, rr);
+      const float dn = dnx - mu;
       const float un = c * g - s * dn;
       dw = fmaf(s, g, c * dn);
       if (i > 0) {
@@ -304,11 +316,18 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
       r1 = rr;
       u1 = un;
       g = c1 * en;
+      ei = en;
+      dnx = dnx2;
+      en = en2;
     }
     Dg[(m - 2) * T + k] = (c1 * (c2 * r1) - s1 * u1) + mu;
     Eg[(m - 2) * T + k] = -s1 * dw;
     Dg[(m - 1) * T + k] = c1 * dw + mu;
-    if (VECS) msw[slot * T + k] = m;
+    if (VECS) {
+      const int padded = min(NMAX - 1, ((m - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk);
+      for (int i = m - 1; i < padded; ++i) rs[i * T] = make_float2(1.0f, 0.0f);
+      msw[slot * T + k] = m;
+    }
   };
 
   for (;;) {
@@ -318,9 +337,9 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
       while (!bfin) {
         if (bm > 2 && bsteps < cfg.max_steps) {
           if (VECS && slot + 2 > S) break;
-          float lo, hi, wc, ws;
-          wilkinson(Dg[(bm - 2) * T + k], Eg[(bm - 2) * T + k], Dg[(bm - 1) * T + k], lo, hi,
-                    wc, ws);
+          float lo, hi;
+          wilkinson_shifts(Dg[(bm - 2) * T + k], Eg[(bm - 2) * T + k], Dg[(bm - 1) * T + k], lo,
+                           hi);
           sweep(k, bm, hi, slot++);
           while (bm > 2 && fabsf(Eg[(bm - 2) * T + k]) < cfg.eps) --bm;
           if (bm > 2) {
@@ -341,7 +360,9 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
           Dg[k] = lo;
           Dg[T + k] = hi;
           if (VECS) {
-            rot[(size_t)slot * (NMAX - 1) * T + k] = make_float2(c, s);
+            float2* rs = rot + (size_t)slot * (NMAX - 1) * T + k;
+            rs[0] = make_float2(c, s);
+            for (int i = 1; i < min(NMAX - 1, kFoldBlk); ++i) rs[i * T] = make_float2(1.0f, 0.0f);
             msw[slot * T + k] = 2;
             ++slot;
           }
@@ -355,21 +376,27 @@ __global__ void __launch_bounds__(MedParams<NMAX, T_, S_>::THREADS, 1)
     }
     if (!VECS) break;
     __syncthreads();
-    // fold the chunk's rotations into the owned V row
+    // fold the chunk's rotations into the owned V row, kFoldBlk positions at
+    // a time (static register indices; the band lane padded each sweep with
+    // identity rotations up to a block boundary)
     if (mlive) {
 #pragma unroll 1
       for (int s2 = 0; s2 < S; ++s2) {
         const int m = msw[s2 * T + mi];
         if (m == 0) break;
         const float2* rs = rot + (size_t)s2 * (NMAX - 1) * T + mi;
+        static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bc) {
+          constexpr int b0 = decltype(bc)::value * kFoldBlk;
+          if (b0 < m - 1) {
 #pragma unroll
-        for (int p = 0; p < NMAX - 1; ++p) {
-          if (p >= m - 1) break;
-          const float2 cs = rs[p * T];
-          const float x = v[p], y = v[p + 1];
-          v[p] = cs.x * x - cs.y * y;
-          v[p + 1] = fmaf(cs.y, x, cs.x * y);
-        }
+            for (int p = b0; p < (b0 + kFoldBlk < NMAX - 1 ? b0 + kFoldBlk : NMAX - 1); ++p) {
+              const float2 cs = rs[p * T];
+              const float x = v[p], y = v[p + 1];
+              v[p] = cs.x * x - cs.y * y;
+              v[p + 1] = fmaf(cs.y, x, cs.x * y);
+            }
+          }
+        });
       }
     }
     const int more = __syncthreads_or(band_lane && !bfin);

@@ -9,6 +9,12 @@
 // compile-time constant (loops fully unrolled on N, the per-matrix active
 // size m is a runtime predicate), so nothing spills to local memory.
 //
+// The QR loop runs warp-synchronously: all 32 lanes stay in the loop until
+// every lane's matrix has deflated, finished lanes run masked (no-op) sweeps,
+// and sweep positions beyond every lane's active block are skipped by a warp
+// vote.  That keeps the code straight-line (no per-lane control flow the
+// compiler could fold into dynamically indexed, local-memory register arrays).
+//
 // Per-matrix pipeline (reference /root/reference/pkg/src/batchedeig):
 //   validate + symmetrise        core.py:286-309
 //   Householder reduction        _kernels.py:36-92, with V <- V H_i folded
@@ -50,25 +56,28 @@ BED_HD void small_fold(float (&v)[N][N], int p, float c, float s) {
     for (int r = 0; r < N; ++r) {
       float x = v[r][p], y = v[r][p + 1];
       v[r][p] = c * x - s * y;
-      v[r][p + 1] = s * x + c * y;
+      v[r][p + 1] = fmaf(s, x, c * y);
     }
   }
 }
 
+__device__ __forceinline__ bool warp_any(bool p) { return __any_sync(0xffffffffu, p); }
+
 // One explicit shifted QR sweep of the leading m-block, fused exactly like
-// _sweep_block (rotation i-1 retires once rotation i exists).  Written as
-// straight-line predicated code over all N positions: rotations at
-// positions >= m-1 degenerate to the identity (a zero target gives c=1,
-// s=0 exactly, _kernels.py:247) and writes past the active block are
-// masked with selects.  Control flow that depends on m would let the
-// compiler merge the per-position blocks into one dynamically indexed block,
-// which demotes d, e and V to local memory.
+// _sweep_block (rotation i-1 retires once rotation i exists), written as
+// predicated straight-line code: rotations at positions >= m-1 degenerate to
+// the identity (a zero target gives c=1, s=0 exactly, _kernels.py:247) and
+// writes past the active block are masked with selects.  m = 0 makes the
+// whole sweep a no-op (used for lanes whose matrix has finished).  Position
+// i is skipped outright when no lane of the warp needs it.
 template <int N, bool VECS>
-BED_HD void small_sweep(float (&d)[N], float (&e)[N], float (&v)[N][N], int m, float mu) {
+__device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N], float (&v)[N][N],
+                                            int m, float mu) {
   float dw = d[0] - mu, g = e[0];
   float c1 = 1.0f, s1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
+    if (i >= 2 && !warp_any(i <= m - 1)) break;
     const bool act = i < m - 1;
     const float ei = (i < N - 1 && act) ? e[i] : 0.0f;
     float c, s, r;
@@ -83,7 +92,7 @@ BED_HD void small_sweep(float (&d)[N], float (&e)[N], float (&v)[N][N], int m, f
       e[i - 1] = wr ? -s1 * r : e[i - 1];
       small_fold<N, VECS>(v, i - 1, c1, s1);  // identity once past the block
     }
-    if (i == m - 1) d[i] = c1 * dw + mu;
+    d[i] = (i == m - 1) ? c1 * dw + mu : d[i];
     c2 = c1;
     c1 = c;
     s1 = s;
@@ -183,21 +192,24 @@ __global__ void __launch_bounds__(kSmallThreads)
 #pragma unroll
     for (int r = i + 1; r < N; ++r) scale = fmaxf(scale, fabsf(a[r][i]));
     if (scale > kZeroTail) {
-      float is = 1.0f / scale;
+      // reflector of the scaled tail xs = tail/scale (householder.py:97-118):
+      // sigma_s = sign(xs_0) ||xs||, u0 = xs_0 + sigma_s, ||u||^2 = 2 sigma_s u0
+      const float is = rcp_fast(scale);
+      float u[N];
       float sumsq = 0.0f;
 #pragma unroll
-      for (int r = i + 1; r < N; ++r) {
-        float t = a[r][i] * is;
-        sumsq = fmaf(t, t, sumsq);
+      for (int r = 0; r < N; ++r) {
+        u[r] = r <= i ? 0.0f : a[r][i] * is;
+        sumsq = fmaf(u[r], u[r], sumsq);
       }
-      float norm = scale * sqrtf(sumsq);
-      float pivot = a[i + 1][i];
-      float sigma = pivot >= 0.0f ? norm : -norm;
-      float u0 = pivot + sigma;
-      float iu = 1.0f / (sqrtf(2.0f * fabsf(sigma)) * sqrtf(fabsf(u0)));
-      float u[N];
+      const float pivot = u[i + 1];
+      const float nrm = sumsq * rsqrt_nr(sumsq);
+      const float sigma = pivot >= 0.0f ? nrm : -nrm;
+      const float u0 = pivot + sigma;
+      const float iu = rsqrt_nr(2.0f * sigma * u0);  // sigma, u0 share a sign
+      u[i + 1] = u0;
 #pragma unroll
-      for (int r = 0; r < N; ++r) u[r] = r <= i ? 0.0f : (r == i + 1 ? u0 : a[r][i]) * iu;
+      for (int r = i + 1; r < N; ++r) u[r] *= iu;
       // p = 2 A u on rows i.., K = u^T p, q = p - K u  (u_i = 0)
       float q[N];
       float kk = 0.0f;
@@ -223,9 +235,9 @@ __global__ void __launch_bounds__(kSmallThreads)
           float t = 0.0f;
 #pragma unroll
           for (int c = i + 1; c < N; ++c) t = fmaf(v[r][c], u[c], t);
-          t *= 2.0f;
+          t *= -2.0f;
 #pragma unroll
-          for (int c = i + 1; c < N; ++c) v[r][c] = fmaf(-t, u[c], v[r][c]);
+          for (int c = i + 1; c < N; ++c) v[r][c] = fmaf(t, u[c], v[r][c]);
         }
       }
     }
@@ -241,25 +253,26 @@ __global__ void __launch_bounds__(kSmallThreads)
   float top = 0.0f;
 #pragma unroll
   for (int j = 0; j < N; ++j) top = fmaxf(top, fmaxf(fabsf(d[j]), fabsf(e[j])));
-  const float scale = pow2_ceil(top);
-  const float iscale = 1.0f / scale;  // exact: power of two
+  float iscale;
+  const float scale = pow2_ceil(top, &iscale);  // exact powers of two
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     d[j] *= iscale;
     e[j] *= iscale;
   }
 
-  // ---- double-shift QR with per-matrix deflation
+  // ---- double-shift QR with per-matrix deflation, warp-synchronous
   int steps = 0;
   if constexpr (N >= 3) {
     int m = small_deflate<N>(e, N, cfg.eps);
-    while (m > 2) {
-      if (steps >= cfg.max_steps) {
+    bool run = m > 2;
+    while (warp_any(run)) {
+      if (run && steps >= cfg.max_steps) {  // budget exhausted: qr.py:604-612
         float resid = 0.0f;
 #pragma unroll
         for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
         if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
-        break;  // lock the diagonal; the leading 2x2 still closes below
+        run = false;  // lock the diagonal; the leading 2x2 still closes below
       }
       // trailing 2x2 of the active block; an arithmetic blend, not a select
       // chain, so the compiler cannot fold it into a dynamically indexed
@@ -272,19 +285,20 @@ __global__ void __launch_bounds__(kSmallThreads)
         tb = fmaf(w, e[j], tb);
         td = fmaf(w, d[j + 1], td);
       }
-      float lo, hi, wc, ws;
-      wilkinson(ta, tb, td, lo, hi, wc, ws);
-      small_sweep<N, VECS>(d, e, v, m, hi);
-      m = small_deflate<N>(e, m, cfg.eps);
-      if (m > 2) {
-        small_sweep<N, VECS>(d, e, v, m, lo);
+      float lo, hi;
+      wilkinson_shifts(ta, tb, td, lo, hi);
+      small_sweep<N, VECS>(d, e, v, run ? m : 0, hi);
+      if (run) m = small_deflate<N>(e, m, cfg.eps);
+      small_sweep<N, VECS>(d, e, v, (run && m > 2) ? m : 0, lo);
+      if (run) {
         m = small_deflate<N>(e, m, cfg.eps);
+        ++steps;
+        run = m > 2;
       }
-      ++steps;
     }
   }
   if constexpr (N >= 2) {
-    float lo, hi, c, s;
+    float lo, hi, c, s;  // exact 2x2 closeout (_kernels.py:401-417)
     wilkinson(d[0], e[0], d[1], lo, hi, c, s);
     d[0] = lo;
     d[1] = hi;
