@@ -6,9 +6,11 @@
  *
  * Plain pointers and sizes only.  Device entry points take device pointers
  * and a CUDA stream (cudaStream_t passed as void*), are asynchronous and
- * stream-ordered, allocate nothing and keep no global mutable state
- * (reentrant; one call per device stream).  The host entry point takes host
- * pointers and does the copies itself.
+ * stream-ordered and reentrant (one call per device stream).  For n <= 8
+ * they allocate nothing; for n >= 9 the forward takes a workspace (at most
+ * 1 GiB, reused chunk by chunk) from the device's stream-ordered memory pool
+ * (cudaMallocAsync / cudaFreeAsync on the same stream).  The host entry
+ * point takes host pointers and does the copies itself.
  *
  * Reference interfaces each entry point replaces (paths relative to the
  * reference package root /root/reference/pkg/src/batchedeig):

@@ -49,11 +49,26 @@ bed::KernelCfg kernel_cfg(const bed_config* cfg, int n) {
   return k;
 }
 
+// The n >= 9 path takes its workspace from the device's stream-ordered
+// memory pool; keep freed blocks cached in the pool across calls.
+void keep_pool_warm() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 cudaError_t dispatch_forward(const bed::FwdArgs& a) {
+  if (a.n > 8) keep_pool_warm();
   if (a.n <= 8) return bed::launch_small(a);
-  if (a.n <= 16) return bed::launch_medium16(a);
-  if (a.n <= 32) return bed::launch_medium32(a);
-  return bed::launch_medium64(a);
+  if (a.n <= 16) return bed::launch_split16(a);
+  if (a.n <= 32) return bed::launch_split32(a);
+  return bed::launch_split64(a);
 }
 
 }  // namespace

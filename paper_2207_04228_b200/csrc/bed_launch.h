@@ -35,9 +35,9 @@ struct BwdArgs {
 };
 
 cudaError_t launch_small(const FwdArgs& a);      // 1 <= n <= 8   (bed_small.cu)
-cudaError_t launch_medium16(const FwdArgs& a);   // 9 <= n <= 16  (bed_medium16.cu)
-cudaError_t launch_medium32(const FwdArgs& a);   // 17 <= n <= 32 (bed_medium32.cu)
-cudaError_t launch_medium64(const FwdArgs& a);   // 33 <= n <= 64 (bed_medium64.cu)
+cudaError_t launch_split16(const FwdArgs& a);    // 9 <= n <= 16  (bed_split16.cu)
+cudaError_t launch_split32(const FwdArgs& a);    // 17 <= n <= 32 (bed_split32.cu)
+cudaError_t launch_split64(const FwdArgs& a);    // 33 <= n <= 64 (bed_split64.cu)
 cudaError_t launch_backward(const BwdArgs& a);   // 1 <= n <= 64  (bed_backward.cu)
 
 }  // namespace bed

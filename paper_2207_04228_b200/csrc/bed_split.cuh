@@ -1,0 +1,525 @@
+// bed_split.cuh -- forward ED for 9 <= n <= 64 as three kernels per chunk.
+//
+// The band QR iteration is a long chain of dependent scalar rotations
+// (~1.2 n^2 per matrix, each ~50 cycles of latency), while the eigenvector
+// fold is wide, cheap arithmetic on n x n registers.  Running both in one
+// kernel ties the number of matrices whose chains can overlap to how many
+// V's fit in the register file.  So the work is split:
+//
+//   H (bed_hh_kernel)    lane group per matrix (lane r owns row r):
+//                        validate + symmetrise (core.py:286-309), Householder
+//                        reduction (_kernels.py:36-92) with reflectors as
+//                        shared-memory broadcasts, P = H_0 H_1 ... formed row
+//                        by row (householder.py:216-231).  Writes P (the
+//                        initial V) and the band (position-major) to the
+//                        workspace.
+//   Q (bed_qr_kernel)    one THREAD per matrix, the band in registers:
+//                        equilibration (qr.py:522-534), double-shift sweeps
+//                        (_sweep_block, _kernels.py:221-300) with per-matrix
+//                        deflation (qr_loop_kernel :321-398 with the gate of
+//                        :381-388), 2x2 closeout (:401-417).  Thousands of
+//                        independent chains per SM hide the latency.  Every
+//                        rotation (c, s) is streamed to the workspace as
+//                        [warp][sweep][position][lane] -- one coalesced
+//                        256-byte store per warp and position.
+//   F (bed_fold_kernel)  lane group per matrix: V := P, then the recorded
+//                        rotations applied to V's rows in registers (two
+//                        column updates, _kernels.py:269-277), then stable
+//                        sort + sign (solver.py:60-76) and coalesced stores.
+//
+// Values-only solves (solver.py:94-109) run H (band only) and Q, which sorts
+// the eigenvalues itself.
+#pragma once
+
+#include "bed_group.cuh"
+
+namespace bed {
+
+constexpr int kFoldBlk = 8;    // positions per static fold block
+constexpr int kQThreads = 128;
+
+struct SplitWs {
+  float* P;         // [bc][n][n] initial V (VECS)
+  float* D;         // [n][Bc] band diagonal, position-major
+  float* E;         // [n][Bc] band off-diagonal
+  float* lam;       // [n][Bc] unsorted eigenvalues (VECS)
+  int32_t* vstat;   // [Bc] validation status from H
+  float2* rot;      // [W][Smax][NMAX-1][32] recorded rotations (VECS)
+  int32_t* msw;     // [W][Smax] warp-maximum active size of each recorded sweep
+  int32_t* nsw;     // [W] sweeps recorded by warp w
+  int64_t Bc;       // chunk capacity (multiple of 32)
+  int Smax;         // sweep records per warp
+};
+
+template <int NMAX>
+struct HHParams {
+  static constexpr int L = GroupSize<NMAX>::L;
+  static constexpr int G = 256 / L;  // matrices per CTA
+  static constexpr int THREADS = G * L;
+  static constexpr int SROW = NMAX + 1;
+  static constexpr int SMAT = NMAX * SROW;
+  static constexpr int OFF_Q = G * SMAT;
+  static constexpr int OFF_RED = OFF_Q + G * NMAX;
+  static constexpr int TOTAL = OFF_RED + 4 * G;
+  static constexpr size_t BYTES = sizeof(float) * TOTAL;
+};
+
+// ---------------------------------------------------------------------------
+// H: validation, Householder reduction, P.
+template <int NMAX, bool EXACT, bool VECS>
+__global__ void __launch_bounds__(HHParams<NMAX>::THREADS)
+    bed_hh_kernel(const float* __restrict__ A, int64_t bc, int n_rt, SplitWs ws, KernelCfg cfg) {
+  using P = HHParams<NMAX>;
+  constexpr int L = P::L, G = P::G;
+  const int n = EXACT ? NMAX : n_rt;
+  const int nn = n * n;
+  extern __shared__ __align__(16) float smem[];
+  const int tid = threadIdx.x;
+  const int mi = tid / L;
+  const int r = tid % L;
+  Group<L> grp;
+  grp.init(tid, mi, smem + P::OFF_RED + 4 * mi);
+  const int64_t j0 = (int64_t)blockIdx.x * G;
+  const int count = (bc - j0) < G ? (int)(bc - j0) : G;
+  const bool mlive = mi < count;
+  const int64_t j = j0 + mi;
+  float* st = smem + mi * P::SMAT;
+  float* qrow = smem + P::OFF_Q + mi * NMAX;
+
+  {  // coalesced tile load into the padded stage
+    const float* src = A + j0 * nn;
+    for (int g = tid; g < count * nn; g += P::THREADS) {
+      int mat = g / nn, off = g - mat * nn;
+      int rr = off / n, c = off - rr * n;
+      smem[mat * P::SMAT + rr * P::SROW + c] = __ldg(src + g);
+    }
+  }
+  __syncthreads();
+
+  float a[NMAX];
+  int status = kStatusOk;
+  {  // validate + symmetrise (core.py:286-309)
+    bool finite = true;
+    float fro2 = 0.0f, asym = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NMAX; ++c) {
+      float x = 0.0f, y = 0.0f;
+      if (mlive && r < n && c < n) {
+        x = st[r * P::SROW + c];
+        y = st[c * P::SROW + r];
+      }
+      finite = finite && isfinite(x);
+      fro2 = fmaf(x, x, fro2);
+      asym = fmaxf(asym, fabsf(x - y));
+      a[c] = 0.5f * (x + y);
+    }
+    finite = grp.max(finite ? 0.0f : 1.0f) == 0.0f;
+    fro2 = grp.sum(fro2);
+    asym = grp.max(asym);
+    if (!finite) status = kStatusNonFinite;
+    else if (asym > cfg.sym_tol * fmaxf(1.0f, sqrtf(fro2))) status = kStatusNonSym;
+    if (status != kStatusOk) {
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c) a[c] = 0.0f;
+    }
+  }
+  grp.sync();  // stage rows are about to be reused for reflectors
+
+  // Householder reduction, reflector i stored in st[i][*].  The step loop is
+  // expanded by template recursion: NVVM's unroller gives up on the n = 64
+  // body and would demote the row to local memory.
+  static_for<0, NMAX - 2>([&](auto ic) {
+    constexpr int i = decltype(ic)::value;
+    if (!EXACT && i >= n - 2) return;
+    const float x = r > i ? a[i] : 0.0f;
+    const float scale = grp.max(fabsf(x));
+    float* urow = st + i * P::SROW;
+    if (scale > kZeroTail) {
+      // reflector of the scaled tail xs = tail/scale (householder.py:97-118):
+      // sigma = sign(xs_0) ||xs||, u0 = xs_0 + sigma, ||u||^2 = 2 sigma u0
+      const float xs = x * rcp_fast(scale);
+      const float ss = grp.sum(xs * xs);
+      const float pivot = grp.bcast(xs, i + 1);
+      const float nrm = ss * rsqrt_nr(ss);
+      const float sigma = pivot >= 0.0f ? nrm : -nrm;
+      const float u0 = pivot + sigma;
+      const float iu = rsqrt_nr(2.0f * sigma * u0);  // sigma, u0 share a sign
+      const float u = (r == i + 1 ? u0 : xs) * iu;   // xs = 0 for r <= i
+      if (r < NMAX) urow[r] = u;
+      grp.sync();
+      // p = 2 A u, K = u^T p, q = p - K u (zero above row i)
+      float p = 0.0f;
+#pragma unroll
+      for (int c = i + 1; c < NMAX; ++c) p = fmaf(a[c], urow[c], p);
+      p *= 2.0f;
+      const float kk = grp.sum(u * p);
+      const float q = r >= i ? fmaf(-kk, u, p) : 0.0f;
+      if (r < NMAX) qrow[r] = q;
+      grp.sync();
+      if (r >= i) {
+#pragma unroll
+        for (int c = i; c < NMAX; ++c) {
+          const float uc = c > i ? urow[c] : 0.0f;
+          a[c] -= fmaf(q, uc, u * qrow[c]);
+        }
+      }
+    } else if (r < NMAX) {
+      urow[r] = 0.0f;
+    }
+    grp.sync();
+  });
+  // band: D[r] = a(r, r), E[r-1] = a(r, r-1), extracted with an arithmetic
+  // blend so no register array is indexed at run time
+  if (mlive) {
+    float dv = 0.0f, ev = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NMAX; ++c) {
+      dv = fmaf(r == c ? 1.0f : 0.0f, a[c], dv);
+      ev = fmaf(r == c + 1 ? 1.0f : 0.0f, a[c], ev);
+    }
+    if (r < n) ws.D[(int64_t)r * ws.Bc + j] = dv;
+    if (r >= 1 && r < n) ws.E[(int64_t)(r - 1) * ws.Bc + j] = ev;
+    if (r == 0) ws.vstat[j] = status;
+  }
+  if constexpr (VECS) {
+    // P = H_0 H_1 ..., row r in registers
+    float v[NMAX];
+#pragma unroll
+    for (int c = 0; c < NMAX; ++c) v[c] = (r == c) ? 1.0f : 0.0f;
+    static_for<0, NMAX - 2>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if (!EXACT && i >= n - 2) return;
+      const float* urow = st + i * P::SROW;
+      float t = 0.0f;
+#pragma unroll
+      for (int c = i + 1; c < NMAX; ++c) t = fmaf(v[c], urow[c], t);
+      t *= -2.0f;
+#pragma unroll
+      for (int c = i + 1; c < NMAX; ++c) v[c] = fmaf(t, urow[c], v[c]);
+    });
+    grp.sync();  // all reflectors read
+    if (r < n) {
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c)
+        if (c < n) st[r * P::SROW + c] = v[c];
+    }
+    __syncthreads();
+    float* dst = ws.P + j0 * nn;
+    for (int g = tid; g < count * nn; g += P::THREADS) {
+      int mat = g / nn, off = g - mat * nn;
+      int rr = off / n, c = off - rr * n;
+      dst[g] = smem[mat * P::SMAT + rr * P::SROW + c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Q: one thread per matrix, band in registers, warp-synchronous sweeps.
+
+// Fused sweep of the leading m-block (_sweep_block), predicated straight-line
+// code over all NMAX positions (rotations past a lane's block are exact
+// identities; m = 0 is a no-op); positions no lane of the warp needs are
+// skipped by a vote.  Returns the warp's processed extent.  With VECS every
+// rotation is stored to rec[p * 32].
+template <int NMAX, bool VECS>
+__device__ __forceinline__ int qr_sweep(float (&d)[NMAX], float (&e)[NMAX], int m, float mu,
+                                        float2* __restrict__ rec) {
+  float dw = d[0] - mu, g = e[0];
+  float c1 = 1.0f, s1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
+  int extent = NMAX;
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    if (i >= 2 && !__any_sync(0xffffffffu, i <= m - 1)) {
+      extent = i;
+      break;
+    }
+    const bool act = i < m - 1;
+    const float ei = (i < NMAX - 1 && act) ? e[i] : 0.0f;
+    float c, s, r;
+    givens(dw, ei, c, s, r);
+    if (VECS && i < NMAX - 1) rec[i * 32] = make_float2(c, s);
+    const float dn = (i + 1 < NMAX ? d[i + 1] : 0.0f) - mu;
+    const float un = c * g - s * dn;
+    const float dwn = fmaf(s, g, c * dn);
+    if (i > 0) {
+      const bool wr = i <= m - 1;  // rotation i-1 was a real one
+      const float dret = (c1 * (c2 * r1) - s1 * u1) + mu;
+      d[i - 1] = wr ? dret : d[i - 1];
+      e[i - 1] = wr ? -s1 * r : e[i - 1];
+    }
+    d[i] = (i == m - 1) ? c1 * dw + mu : d[i];
+    c2 = c1;
+    c1 = c;
+    s1 = s;
+    r1 = r;
+    u1 = un;
+    dw = dwn;
+    if (i + 1 < NMAX - 1) g = c1 * e[i + 1];
+  }
+  return extent;
+}
+
+template <int NMAX>
+__device__ __forceinline__ int qr_deflate(const float (&e)[NMAX], int m, float eps) {
+  unsigned long long small = 0ull;
+#pragma unroll
+  for (int j = 0; j < NMAX - 1; ++j) small |= (fabsf(e[j]) < eps ? 1ull : 0ull) << j;
+  while (m > 2 && ((small >> (m - 2)) & 1ull)) --m;
+  return m;
+}
+
+template <int NMAX, bool EXACT, bool VECS>
+__global__ void __launch_bounds__(kQThreads)
+    bed_qr_kernel(int64_t bc, int64_t c0, int n_rt, SplitWs ws, float* __restrict__ evals,
+                  int32_t* __restrict__ status_out, int32_t* __restrict__ steps_out,
+                  int32_t* __restrict__ flags, KernelCfg cfg) {
+  const int n = EXACT ? NMAX : n_rt;
+  const int64_t j = (int64_t)blockIdx.x * kQThreads + threadIdx.x;
+  const bool live = j < bc;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = j >> 5;  // warp of the chunk
+  if (j - lane >= bc) return;  // whole warp past the chunk: it owns no records
+  float d[NMAX], e[NMAX];
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    d[i] = (live && i < n) ? ws.D[(int64_t)i * ws.Bc + j] : 0.0f;
+    e[i] = (live && i < n - 1) ? ws.E[(int64_t)i * ws.Bc + j] : 0.0f;
+  }
+  int status = live ? ws.vstat[j] : kStatusOk;
+  float top = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) top = fmaxf(top, fmaxf(fabsf(d[i]), fabsf(e[i])));
+  float iscale;
+  const float scale = pow2_ceil(top, &iscale);  // exact powers of two
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    d[i] *= iscale;
+    e[i] *= iscale;
+  }
+
+  float2* recw = VECS ? ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane : nullptr;
+  int* mw_rec = VECS ? ws.msw + (size_t)w * ws.Smax : nullptr;
+  int nrec = 0;
+  // pad a recorded sweep with identities up to the fold block boundary
+  auto pad = [&](int from, int upto) {
+    for (int p = from; p < upto; ++p) recw[((size_t)nrec * (NMAX - 1) + p) * 32] = make_float2(1.0f, 0.0f);
+  };
+  // close a record: `written` positions were stored, the fold will run whole
+  // blocks up to the one containing position mw - 2
+  auto record_end = [&](int mw, int written) {
+    if constexpr (VECS) {
+      const int padded = min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk);
+      pad(min(written, NMAX - 1), padded);
+      if (lane == 0) mw_rec[nrec] = mw;
+      ++nrec;
+    }
+  };
+
+  int steps = 0;
+  int m = qr_deflate<NMAX>(e, n, cfg.eps);
+  bool run = live && m > 2;
+  while (__any_sync(0xffffffffu, run)) {
+    if (run && steps >= cfg.max_steps) {  // budget exhausted: qr.py:604-612
+      float resid = 0.0f;
+#pragma unroll
+      for (int i = 0; i < NMAX - 1; ++i) resid = fmaxf(resid, i < m - 1 ? fabsf(e[i]) : 0.0f);
+      if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
+      run = false;  // lock the diagonal; the leading 2x2 still closes below
+    }
+    if (!__any_sync(0xffffffffu, run)) break;
+    // trailing 2x2 of the active block via an arithmetic blend
+    float ta = 0.0f, tb = 0.0f, td = 0.0f;
+#pragma unroll
+    for (int i = 1; i < NMAX - 1; ++i) {
+      const float wgt = (i == m - 2) ? 1.0f : 0.0f;
+      ta = fmaf(wgt, d[i], ta);
+      tb = fmaf(wgt, e[i], tb);
+      td = fmaf(wgt, d[i + 1], td);
+    }
+    float lo, hi;
+    wilkinson_shifts(ta, tb, td, lo, hi);
+    const int ma = run ? m : 0;
+    const int mwa = __reduce_max_sync(0xffffffffu, ma);
+    qr_sweep<NMAX, VECS>(d, e, ma, hi, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr);
+    record_end(mwa, mwa);
+    if (run) m = qr_deflate<NMAX>(e, m, cfg.eps);
+    const int mb = (run && m > 2) ? m : 0;
+    const int mwb = __reduce_max_sync(0xffffffffu, mb);
+    if (mwb > 2) {
+      qr_sweep<NMAX, VECS>(d, e, mb, lo, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr);
+      record_end(mwb, mwb);
+    }
+    if (run) {
+      m = qr_deflate<NMAX>(e, m, cfg.eps);
+      ++steps;
+      run = m > 2;
+    }
+  }
+  {  // exact 2x2 closeout (_kernels.py:401-417), recorded as a sweep of extent 2
+    float lo, hi, c, s;
+    wilkinson(d[0], e[0], d[1], lo, hi, c, s);
+    d[0] = lo;
+    d[1] = hi;
+    if constexpr (VECS) {
+      recw[(size_t)nrec * (NMAX - 1) * 32] = make_float2(c, s);
+      record_end(2, 1);
+    }
+  }
+  if (VECS && lane == 0) ws.nsw[w] = nrec;
+
+  if (live) {
+    if constexpr (VECS) {
+#pragma unroll
+      for (int i = 0; i < NMAX; ++i)
+        if (i < n) ws.lam[(int64_t)i * ws.Bc + j] = d[i] * scale;
+    } else {  // values only: stable sort in the thread (solver.py:61-66)
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c) {
+        if (c >= n) continue;
+        int rk = c;
+        if (cfg.sort != 0) {
+          rk = 0;
+#pragma unroll
+          for (int k = 0; k < NMAX; ++k)
+            rk += (k < n && k != c && rank_before(d[k], k, d[c], c, cfg.sort)) ? 1 : 0;
+        }
+        evals[(c0 + j) * n + rk] = d[c] * scale;
+      }
+    }
+    if (status_out) status_out[c0 + j] = status;
+    if (steps_out) steps_out[c0 + j] = steps;
+  }
+  if (flags) {
+    unsigned bits = __reduce_or_sync(0xffffffffu, (live && status) ? (1u << status) : 0u);
+    if (lane == 0 && bits) atomicOr(flags, (int)bits);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// F: fold the recorded rotations into V = P, then sort + sign + store.
+template <int NMAX>
+struct FoldParams {
+  static constexpr int L = GroupSize<NMAX>::L;
+  static constexpr int G = NMAX <= 16 ? 32 : (NMAX <= 32 ? 16 : 8);
+  static constexpr int THREADS = G * L;
+  static constexpr int SROW = NMAX + 1;
+  static constexpr int SMAT = NMAX * SROW;
+  static constexpr int OFF_FLIP = G * SMAT;
+  static constexpr int OFF_EV = OFF_FLIP + G * NMAX;
+  static constexpr int OFF_RANK = OFF_EV + G * NMAX;
+  static constexpr int OFF_LAM = OFF_RANK + G * NMAX;
+  static constexpr int TOTAL = OFF_LAM + G * NMAX;
+  static constexpr size_t BYTES = sizeof(float) * TOTAL;
+};
+
+template <int NMAX, bool EXACT>
+__global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
+    bed_fold_kernel(int64_t bc, int64_t c0, int n_rt, SplitWs ws, float* __restrict__ evals,
+                    float* __restrict__ evecs, KernelCfg cfg) {
+  using P = FoldParams<NMAX>;
+  constexpr int L = P::L, G = P::G;
+  const int n = EXACT ? NMAX : n_rt;
+  const int nn = n * n;
+  extern __shared__ __align__(16) float smem[];
+  float* flipv = smem + P::OFF_FLIP;
+  float* evs = smem + P::OFF_EV;
+  int* ranks = reinterpret_cast<int*>(smem + P::OFF_RANK);
+  float* lams = smem + P::OFF_LAM;
+  const int tid = threadIdx.x;
+  const int mi = tid / L;
+  const int r = tid % L;
+  const int64_t j0 = (int64_t)blockIdx.x * G;
+  const int count = (bc - j0) < G ? (int)(bc - j0) : G;
+  const bool mlive = mi < count;
+  const int64_t j = j0 + mi;
+  float* st = smem + mi * P::SMAT;
+
+  if (mlive && r < n) lams[mi * NMAX + r] = ws.lam[(int64_t)r * ws.Bc + j];
+  {  // coalesced P tile -> stage
+    const float* src = ws.P + j0 * nn;
+    for (int g = tid; g < count * nn; g += P::THREADS) {
+      int mat = g / nn, off = g - mat * nn;
+      int rr = off / n, c = off - rr * n;
+      smem[mat * P::SMAT + rr * P::SROW + c] = src[g];
+    }
+  }
+  __syncthreads();
+  float v[NMAX];
+#pragma unroll
+  for (int c = 0; c < NMAX; ++c) v[c] = (mlive && r < n && c < n) ? st[r * P::SROW + c] : 0.0f;
+
+  if (mlive) {
+    const int64_t w = j >> 5;
+    const int lane = (int)(j & 31);
+    const int nrec = ws.nsw[w];
+    const int* mws = ws.msw + (size_t)w * ws.Smax;
+    const float2* recw = ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane;
+#pragma unroll 1
+    for (int s2 = 0; s2 < nrec; ++s2) {
+      const int mw = __ldg(mws + s2);
+      const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
+      static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bcst) {
+        constexpr int b0 = decltype(bcst)::value * kFoldBlk;
+        constexpr int b1 = b0 + kFoldBlk < NMAX - 1 ? b0 + kFoldBlk : NMAX - 1;
+        if (b0 < mw - 1) {
+          float2 cs[b1 - b0];
+#pragma unroll
+          for (int p = b0; p < b1; ++p) cs[p - b0] = __ldg(rs + p * 32);
+#pragma unroll
+          for (int p = b0; p < b1; ++p) {
+            const float x = v[p], y = v[p + 1];
+            v[p] = cs[p - b0].x * x - cs[p - b0].y * y;
+            v[p + 1] = fmaf(cs[p - b0].y, x, cs[p - b0].x * y);
+          }
+        }
+      });
+    }
+  }
+
+  // stable sort + sign (solver.py:60-76), transposed staging, coalesced store
+  if (mlive && r < n) {
+    const float lr = lams[mi * NMAX + r];
+    int rk = r;
+    if (cfg.sort != 0) {
+      rk = 0;
+      for (int k2 = 0; k2 < n; ++k2)
+        rk += (k2 != r && rank_before(lams[mi * NMAX + k2], k2, lr, r, cfg.sort)) ? 1 : 0;
+    }
+    ranks[mi * NMAX + r] = rk;
+    evs[mi * NMAX + rk] = lr;
+  }
+  __syncthreads();
+  if (mlive && r < n) {
+#pragma unroll
+    for (int c = 0; c < NMAX; ++c)
+      if (c < n) st[r * P::SROW + ranks[mi * NMAX + c]] = v[c];
+  }
+  __syncthreads();
+  if (mlive && r < n) {  // sign: largest-magnitude entry of column r >= 0
+    float best = -1.0f, lead = 0.0f;
+    for (int rr = 0; rr < n; ++rr) {
+      const float x = st[rr * P::SROW + r];
+      if (fabsf(x) > best) {
+        best = fabsf(x);
+        lead = x;
+      }
+    }
+    flipv[mi * NMAX + r] = lead < 0.0f ? -1.0f : 1.0f;
+  }
+  __syncthreads();
+  {
+    float* dst = evecs + (c0 + j0) * nn;
+    for (int g = tid; g < count * nn; g += P::THREADS) {
+      int mat = g / nn, off = g - mat * nn;
+      int rr = off / n, c = off - rr * n;
+      dst[g] = smem[mat * P::SMAT + rr * P::SROW + c] * flipv[mat * NMAX + c];
+    }
+    float* dstl = evals + (c0 + j0) * n;
+    for (int g = tid; g < count * n; g += P::THREADS) {
+      int mat = g / n, c = g - mat * n;
+      dstl[g] = evs[mat * NMAX + c];
+    }
+  }
+}
+
+}  // namespace bed

@@ -1,0 +1,89 @@
+// bed_split_launch.cuh -- host side of the three-kernel path: workspace
+// sizing, chunking and launches (one stream, stream-ordered allocation).
+#pragma once
+
+#include <algorithm>
+
+#include "bed_launch.h"
+#include "bed_split.cuh"
+
+namespace bed {
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Workspace budget per call; chunks of the batch are solved in sequence.
+constexpr size_t kSplitWorkspaceBytes = size_t(1) << 30;
+
+template <typename K>
+inline cudaError_t set_smem(K kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int NMAX, bool EXACT>
+cudaError_t run_split(const FwdArgs& a) {
+  const bool vecs = a.evecs != nullptr;
+  const int n = a.n;
+  const int64_t nn = (int64_t)n * n;
+  const int smax = 2 * a.cfg.max_steps + 1;
+  const size_t per = 4 * (2 * (size_t)n) + 4 +
+                     (vecs ? 4 * (size_t)nn + 4 * (size_t)n + (size_t)smax * (NMAX - 1) * 8 : 0);
+  const size_t per_warp = vecs ? (size_t)smax * 4 + 4 : 0;
+  int64_t cap = (int64_t)(kSplitWorkspaceBytes / (per + per_warp / 32 + 1));
+  const int64_t want = (a.batch + 31) / 32 * 32;
+  int64_t Bc = std::max<int64_t>(32, std::min<int64_t>(cap, want) / 32 * 32);
+  const int64_t W = Bc / 32;
+
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const size_t oP = vecs ? take(4 * (size_t)Bc * nn) : 0;
+  const size_t oD = take(4 * (size_t)Bc * n);
+  const size_t oE = take(4 * (size_t)Bc * n);
+  const size_t oL = vecs ? take(4 * (size_t)Bc * n) : 0;
+  const size_t oV = take(4 * (size_t)Bc);
+  const size_t oR = vecs ? take((size_t)W * smax * (NMAX - 1) * 32 * 8) : 0;
+  const size_t oM = vecs ? take((size_t)W * smax * 4) : 0;
+  const size_t oN = vecs ? take((size_t)W * 4) : 0;
+  char* base = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), off, a.stream);
+  if (e != cudaSuccess) return e;
+  SplitWs ws;
+  ws.P = vecs ? reinterpret_cast<float*>(base + oP) : nullptr;
+  ws.D = reinterpret_cast<float*>(base + oD);
+  ws.E = reinterpret_cast<float*>(base + oE);
+  ws.lam = vecs ? reinterpret_cast<float*>(base + oL) : nullptr;
+  ws.vstat = reinterpret_cast<int32_t*>(base + oV);
+  ws.rot = vecs ? reinterpret_cast<float2*>(base + oR) : nullptr;
+  ws.msw = vecs ? reinterpret_cast<int32_t*>(base + oM) : nullptr;
+  ws.nsw = vecs ? reinterpret_cast<int32_t*>(base + oN) : nullptr;
+  ws.Bc = Bc;
+  ws.Smax = smax;
+
+  using HP = HHParams<NMAX>;
+  using FP = FoldParams<NMAX>;
+  auto hk = vecs ? bed_hh_kernel<NMAX, EXACT, true> : bed_hh_kernel<NMAX, EXACT, false>;
+  auto qk = vecs ? bed_qr_kernel<NMAX, EXACT, true> : bed_qr_kernel<NMAX, EXACT, false>;
+  auto fk = bed_fold_kernel<NMAX, EXACT>;
+  if ((e = set_smem(hk, HP::BYTES)) != cudaSuccess) return e;
+  if (vecs && (e = set_smem(fk, FP::BYTES)) != cudaSuccess) return e;
+
+  for (int64_t c0 = 0; c0 < a.batch && e == cudaSuccess; c0 += Bc) {
+    const int64_t bc = std::min<int64_t>(Bc, a.batch - c0);
+    hk<<<(unsigned)((bc + HP::G - 1) / HP::G), HP::THREADS, HP::BYTES, a.stream>>>(
+        a.A + c0 * nn, bc, n, ws, a.cfg);
+    qk<<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0, a.stream>>>(
+        bc, c0, n, ws, a.evals, a.status, a.steps, a.flags, a.cfg);
+    if (vecs)
+      fk<<<(unsigned)((bc + FP::G - 1) / FP::G), FP::THREADS, FP::BYTES, a.stream>>>(
+          bc, c0, n, ws, a.evals, a.evecs, a.cfg);
+    e = cudaGetLastError();
+  }
+  cudaError_t ef = cudaFreeAsync(base, a.stream);
+  return e != cudaSuccess ? e : ef;
+}
+
+}  // namespace bed

@@ -1,0 +1,19 @@
+"""Small ragged-batch solves of every kernel family, for compute-sanitizer
+(memcheck / racecheck / synccheck) runs."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402
+import paper_2207_04228_b200 as bed  # noqa: E402
+
+torch.cuda.set_device(0)
+for n, b in ((3, 130), (4, 131), (8, 129), (9, 37), (16, 161), (24, 70), (32, 33), (40, 19), (64, 35)):
+    a = torch.from_numpy(oracle.gen_spd(b, n, n).astype(np.float32)).cuda().requires_grad_(True)
+    lam, v = bed.eigh(a, bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n))
+    (v.sum() + lam.sum()).backward()
+    bed.batched_eig(a.detach(), bed.SolverConfig(compute_vectors=False, max_double_steps=4 * n))
+torch.cuda.synchronize()
+print("sanitize cases done")
