@@ -280,7 +280,7 @@ def run_ours(args):
         "gpu_launches": args.steps * step.launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak / 1e9,
                      "unit": "GB/s", "frac": achieved / (hbm_peak / 1e9),
-                     "traffic": load_traffic("bed_small_kernel<4,true>"),
+                     "traffic": load_traffic("bed_small_kernel<4,1>"),
                      "kernel": "bed_small_kernel<4, true>", "peak_source": peak_src,
                      "bytes_per_matrix": work_per_matrix(n, "fwd")[1],
                      "fp32_frac_nominal": flops / per_step / FP32_PEAK_NOMINAL},

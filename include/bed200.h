@@ -8,7 +8,7 @@
  * and a CUDA stream (cudaStream_t passed as void*), are asynchronous and
  * stream-ordered and reentrant (one call per device stream).  For n <= 8
  * they allocate nothing; for n >= 9 the forward takes a workspace (at most
- * 1 GiB, reused chunk by chunk) from the device's stream-ordered memory pool
+ * 4 GiB or a quarter of free memory, reused chunk by chunk) from the device's stream-ordered memory pool
  * (cudaMallocAsync / cudaFreeAsync on the same stream).  The host entry
  * point takes host pointers and does the copies itself.
  *

@@ -67,7 +67,7 @@ struct HHParams {
 // ---------------------------------------------------------------------------
 // H: validation, Householder reduction, P.
 template <int NMAX, bool EXACT, bool VECS>
-__global__ void __launch_bounds__(HHParams<NMAX>::THREADS)
+__global__ void __launch_bounds__(HHParams<NMAX>::THREADS, NMAX <= 32 ? 3 : 1)
     bed_hh_kernel(const float* __restrict__ A, int64_t bc, int n_rt, SplitWs ws, KernelCfg cfg) {
   using P = HHParams<NMAX>;
   constexpr int L = P::L, G = P::G;
@@ -156,12 +156,10 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS)
       const float q = r >= i ? fmaf(-kk, u, p) : 0.0f;
       if (r < NMAX) qrow[r] = q;
       grp.sync();
-      if (r >= i) {
+      if (r >= i) {  // A <- A - q u^T - u q^T as two FMAs per entry (u_i = 0)
+        a[i] = fmaf(-u, qrow[i], a[i]);
 #pragma unroll
-        for (int c = i; c < NMAX; ++c) {
-          const float uc = c > i ? urow[c] : 0.0f;
-          a[c] -= fmaf(q, uc, u * qrow[c]);
-        }
+        for (int c = i + 1; c < NMAX; ++c) a[c] = fmaf(-q, urow[c], fmaf(-u, qrow[c], a[c]));
       }
     } else if (r < NMAX) {
       urow[r] = 0.0f;
@@ -397,19 +395,30 @@ __global__ void __launch_bounds__(kQThreads)
 
 // ---------------------------------------------------------------------------
 // F: fold the recorded rotations into V = P, then sort + sign + store.
+//
+// A CTA holds G matrices of ONE band warp (G divides 32), so all its groups
+// replay the same sweep sequence.  Each sweep's rotations for the CTA's
+// lanes ([position][lane] rows of G float2) are copied into shared memory
+// with coalesced loads one sweep ahead (register prefetch, double-buffered
+// shared buffer, one barrier per sweep); the groups then read their
+// rotation as a conflict-free broadcast.
 template <int NMAX>
 struct FoldParams {
   static constexpr int L = GroupSize<NMAX>::L;
-  static constexpr int G = NMAX <= 16 ? 32 : (NMAX <= 32 ? 16 : 8);
+  static constexpr int G = NMAX <= 32 ? 32 : 8;
   static constexpr int THREADS = G * L;
   static constexpr int SROW = NMAX + 1;
   static constexpr int SMAT = NMAX * SROW;
-  static constexpr int OFF_FLIP = G * SMAT;
+  static constexpr int PADPOS = ((NMAX - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk;
+  static constexpr int OFF_ROT = G * SMAT;                         // float2 [2][PADPOS][G]
+  static constexpr int OFF_FLIP = OFF_ROT + 2 * 2 * PADPOS * G;
   static constexpr int OFF_EV = OFF_FLIP + G * NMAX;
   static constexpr int OFF_RANK = OFF_EV + G * NMAX;
   static constexpr int OFF_LAM = OFF_RANK + G * NMAX;
   static constexpr int TOTAL = OFF_LAM + G * NMAX;
   static constexpr size_t BYTES = sizeof(float) * TOTAL;
+  static constexpr int PER_THREAD = (PADPOS * G + THREADS - 1) / THREADS;  // prefetch slots
+  static_assert(32 % G == 0, "a CTA must not straddle band warps");
 };
 
 template <int NMAX, bool EXACT>
@@ -421,6 +430,7 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
   const int n = EXACT ? NMAX : n_rt;
   const int nn = n * n;
   extern __shared__ __align__(16) float smem[];
+  float2* rbuf = reinterpret_cast<float2*>(smem + P::OFF_ROT);
   float* flipv = smem + P::OFF_FLIP;
   float* evs = smem + P::OFF_EV;
   int* ranks = reinterpret_cast<int*>(smem + P::OFF_RANK);
@@ -448,32 +458,63 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
 #pragma unroll
   for (int c = 0; c < NMAX; ++c) v[c] = (mlive && r < n && c < n) ? st[r * P::SROW + c] : 0.0f;
 
-  if (mlive) {
-    const int64_t w = j >> 5;
-    const int lane = (int)(j & 31);
-    const int nrec = ws.nsw[w];
-    const int* mws = ws.msw + (size_t)w * ws.Smax;
-    const float2* recw = ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane;
+  // rotation stream of this CTA's band warp
+  const int64_t w = j0 >> 5;
+  const int lane0 = (int)(j0 & 31);
+  const int nrec = ws.nsw[w];
+  const int* mws = ws.msw + (size_t)w * ws.Smax;
+  const float2* recw = ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane0;
+  // thread t stages elements t, t + THREADS, ... of the [PADPOS][G] block
+  float2 pf[P::PER_THREAD];
+  auto fetch = [&](int s2, int npos) {
+    const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
+#pragma unroll
+    for (int q = 0; q < P::PER_THREAD; ++q) {
+      const int e = tid + q * P::THREADS;
+      const int p = e / G, g = e - p * G;
+      pf[q] = (p < npos) ? __ldg(rs + p * 32 + g) : make_float2(1.0f, 0.0f);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < P::PER_THREAD; ++q) {
+      const int e = tid + q * P::THREADS;
+      if (e < P::PADPOS * G) rbuf[buf * P::PADPOS * G + e] = pf[q];
+    }
+  };
+  auto npos_of = [&](int mw) { return min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk); };
+  int mw_next = nrec > 0 ? __ldg(mws) : 0;
+  if (nrec > 0) {
+    fetch(0, npos_of(mw_next));
+    stash(0);
+  }
+  __syncthreads();
 #pragma unroll 1
-    for (int s2 = 0; s2 < nrec; ++s2) {
-      const int mw = __ldg(mws + s2);
-      const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
+  for (int s2 = 0; s2 < nrec; ++s2) {
+    const int buf = s2 & 1;
+    const int mw = mw_next;
+    if (s2 + 1 < nrec) {  // prefetch the next sweep while this one is folded
+      mw_next = __ldg(mws + s2 + 1);
+      fetch(s2 + 1, npos_of(mw_next));
+    }
+    if (mlive) {
+      const float2* rs = rbuf + buf * P::PADPOS * G + mi;
       static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bcst) {
         constexpr int b0 = decltype(bcst)::value * kFoldBlk;
         constexpr int b1 = b0 + kFoldBlk < NMAX - 1 ? b0 + kFoldBlk : NMAX - 1;
         if (b0 < mw - 1) {
-          float2 cs[b1 - b0];
-#pragma unroll
-          for (int p = b0; p < b1; ++p) cs[p - b0] = __ldg(rs + p * 32);
 #pragma unroll
           for (int p = b0; p < b1; ++p) {
+            const float2 cs = rs[p * G];
             const float x = v[p], y = v[p + 1];
-            v[p] = cs[p - b0].x * x - cs[p - b0].y * y;
-            v[p + 1] = fmaf(cs[p - b0].y, x, cs[p - b0].x * y);
+            v[p] = cs.x * x - cs.y * y;
+            v[p + 1] = fmaf(cs.y, x, cs.x * y);
           }
         }
       });
     }
+    if (s2 + 1 < nrec) stash(buf ^ 1);
+    __syncthreads();
   }
 
   // stable sort + sign (solver.py:60-76), transposed staging, coalesced store

@@ -12,7 +12,7 @@ namespace bed {
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Workspace budget per call; chunks of the batch are solved in sequence.
-constexpr size_t kSplitWorkspaceBytes = size_t(1) << 30;
+constexpr size_t kSplitWorkspaceBytes = size_t(4) << 30;
 
 template <typename K>
 inline cudaError_t set_smem(K kern, size_t bytes) {
@@ -29,8 +29,14 @@ cudaError_t run_split(const FwdArgs& a) {
   const size_t per = 4 * (2 * (size_t)n) + 4 +
                      (vecs ? 4 * (size_t)nn + 4 * (size_t)n + (size_t)smax * (NMAX - 1) * 8 : 0);
   const size_t per_warp = vecs ? (size_t)smax * 4 + 4 : 0;
-  int64_t cap = (int64_t)(kSplitWorkspaceBytes / (per + per_warp / 32 + 1));
   const int64_t want = (a.batch + 31) / 32 * 32;
+  const size_t need = (size_t)want * (per + per_warp / 32 + 1);
+  size_t budget = kSplitWorkspaceBytes;
+  if (need > (size_t(256) << 20)) {  // only large solves pay for the free-memory query
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min(budget, free_b / 4);
+  }
+  int64_t cap = (int64_t)(budget / (per + per_warp / 32 + 1));
   int64_t Bc = std::max<int64_t>(32, std::min<int64_t>(cap, want) / 32 * 32);
   const int64_t W = Bc / 32;
 
@@ -68,8 +74,16 @@ cudaError_t run_split(const FwdArgs& a) {
   auto hk = vecs ? bed_hh_kernel<NMAX, EXACT, true> : bed_hh_kernel<NMAX, EXACT, false>;
   auto qk = vecs ? bed_qr_kernel<NMAX, EXACT, true> : bed_qr_kernel<NMAX, EXACT, false>;
   auto fk = bed_fold_kernel<NMAX, EXACT>;
-  if ((e = set_smem(hk, HP::BYTES)) != cudaSuccess) return e;
-  if (vecs && (e = set_smem(fk, FP::BYTES)) != cudaSuccess) return e;
+  static bool attrs_set = false;  // idempotent; a benign race at worst repeats it
+  if (!attrs_set) {
+    if ((e = set_smem(bed_hh_kernel<NMAX, EXACT, true>, HP::BYTES)) != cudaSuccess ||
+        (e = set_smem(bed_hh_kernel<NMAX, EXACT, false>, HP::BYTES)) != cudaSuccess ||
+        (e = set_smem(fk, FP::BYTES)) != cudaSuccess) {
+      cudaFreeAsync(base, a.stream);
+      return e;
+    }
+    attrs_set = true;
+  }
 
   for (int64_t c0 = 0; c0 < a.batch && e == cudaSuccess; c0 += Bc) {
     const int64_t bc = std::min<int64_t>(Bc, a.batch - c0);
