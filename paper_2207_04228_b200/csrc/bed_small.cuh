@@ -9,6 +9,12 @@
 // compile-time constant (loops fully unrolled on N, the per-matrix active
 // size m is a runtime predicate), so nothing spills to local memory.
 //
+// The kernel is limited by instruction issue (n = 4: ~90 % issue-active,
+// FMA pipe ~50 %), so V is held as packed row pairs (bed_f32x2.cuh): a
+// Givens fold on two columns costs 2 FFMA2 + 2 FMUL2 per two rows instead
+// of 8 scalar ops, and the band recurrence computes its (u, dw) pair with
+// one FMUL2 + one FFMA2.
+//
 // The QR loop runs warp-synchronously: all 32 lanes stay in the loop until
 // every lane's matrix has deflated, finished lanes run masked (no-op) sweeps,
 // and sweep positions beyond every lane's active block are skipped by a warp
@@ -31,6 +37,7 @@
 #pragma once
 
 #include "bed_common.cuh"
+#include "bed_f32x2.cuh"
 
 namespace bed {
 
@@ -39,6 +46,7 @@ constexpr int kSmallThreads = 128;
 template <int N>
 struct SmallLayout {
   static constexpr int NN = N * N;
+  static constexpr int NP = (N + 1) / 2;                 // packed row pairs of V
   static constexpr int STRIDE = (NN % 2) ? NN : NN + 1;  // odd => conflict free
   static constexpr int LSTRIDE = (N % 2) ? N : N + 1;
 };
@@ -49,68 +57,90 @@ BED_HD float sym_at(const float (&a)[N][N], int r, int c) {
   return c <= r ? a[r][c] : a[c][r];
 }
 
+// V(r, c) of the packed row-pair store.
+template <int NP, int N>
+__device__ __forceinline__ float v_at(const f2 (&v)[NP][N], int r, int c) {
+  return (r & 1) ? f2_hi(v[r >> 1][c]) : f2_lo(v[r >> 1][c]);
+}
+
+// V <- V R on columns (p, p+1), all rows; an identity rotation (c = 1,
+// s = 0) leaves V bit-identical.
 template <int N, bool VECS>
-BED_HD void small_fold(float (&v)[N][N], int p, float c, float s) {
+__device__ __forceinline__ void small_fold(f2 (&v)[SmallLayout<N>::NP][N], int p, float c,
+                                           float s, float ns) {
   if constexpr (VECS) {
 #pragma unroll
-    for (int r = 0; r < N; ++r) {
-      float x = v[r][p], y = v[r][p + 1];
-      v[r][p] = c * x - s * y;
-      v[r][p + 1] = fmaf(s, x, c * y);
-    }
+    for (int rp = 0; rp < SmallLayout<N>::NP; ++rp) rot2(v[rp][p], v[rp][p + 1], c, s, ns);
   }
 }
 
 __device__ __forceinline__ bool warp_any(bool p) { return __any_sync(0xffffffffu, p); }
 
+// Givens rotation of the fused sweep with the identity rule folded into the
+// inputs: a dead target (|e| < 2^-60, or a position past the active block,
+// passed as e = 0) runs on (1, 0), giving c = 1, s = 0 exactly; r is then
+// the unrotated dw (_kernels.py:247, :256-258).
+__device__ __forceinline__ void small_givens(float dw, float e, float& c, float& s, float& ns,
+                                             float& r) {
+  const bool live = fabsf(e) >= 0x1p-60f;
+  const float x = live ? dw : 1.0f;
+  const float y = live ? e : 0.0f;
+  const float h2 = fmaf(x, x, y * y);
+  const float ih = rsqrt_nr(h2);
+  c = x * ih;
+  s = -y * ih;
+  ns = y * ih;
+  const float rr = h2 * ih;
+  r = live ? rr : dw;
+}
+
 // One explicit shifted QR sweep of the leading m-block, fused exactly like
 // _sweep_block (rotation i-1 retires once rotation i exists), written as
 // predicated straight-line code: rotations at positions >= m-1 degenerate to
-// the identity (a zero target gives c=1, s=0 exactly, _kernels.py:247) and
-// writes past the active block are masked with selects.  m = 0 makes the
-// whole sweep a no-op (used for lanes whose matrix has finished).  Position
-// i is skipped outright when no lane of the warp needs it.
+// the identity and writes past the active block are masked with selects.
+// m = 0 makes the whole sweep a no-op (used for lanes whose matrix has
+// finished).  Position i is skipped outright when no lane of the warp needs
+// it.
 template <int N, bool VECS>
-__device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N], float (&v)[N][N],
-                                            int m, float mu) {
+__device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N],
+                                            f2 (&v)[SmallLayout<N>::NP][N], int m, float mu) {
   float dw = d[0] - mu, g = e[0];
-  float c1 = 1.0f, s1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
+  float c1 = 1.0f, s1 = 0.0f, ns1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     if (i >= 2 && !warp_any(i <= m - 1)) break;
     const bool act = i < m - 1;
     const float ei = (i < N - 1 && act) ? e[i] : 0.0f;
-    float c, s, r;
-    givens(dw, ei, c, s, r);
+    float c, s, ns, r;
+    small_givens(dw, ei, c, s, ns, r);
     const float dn = (i + 1 < N ? d[i + 1] : 0.0f) - mu;
-    const float un = c * g - s * dn;
-    const float dwn = fmaf(s, g, c * dn);
+    // (u, dw') = (c g - s dn, s g + c dn)
+    const f2 ud = ffma2(f2_make(ns, c), f2_bc(dn), fmul2(f2_make(c, s), f2_bc(g)));
     if (i > 0) {
       const bool wr = i <= m - 1;  // rotation i-1 was a real one
       const float dret = (c1 * (c2 * r1) - s1 * u1) + mu;
       d[i - 1] = wr ? dret : d[i - 1];
-      e[i - 1] = wr ? -s1 * r : e[i - 1];
-      small_fold<N, VECS>(v, i - 1, c1, s1);  // identity once past the block
+      e[i - 1] = wr ? ns1 * r : e[i - 1];
+      small_fold<N, VECS>(v, i - 1, c1, s1, ns1);  // identity once past the block
     }
     d[i] = (i == m - 1) ? c1 * dw + mu : d[i];
     c2 = c1;
     c1 = c;
     s1 = s;
+    ns1 = ns;
     r1 = r;
-    u1 = un;
-    dw = dwn;
+    u1 = f2_lo(ud);
+    dw = f2_hi(ud);
     if (i + 1 < N - 1) g = c1 * e[i + 1];
   }
 }
 
-// Trailing deflation: while m > 2 and |e[m-2]| < eps, m -= 1 -- on a bit
-// mask of the small couplings, so no array is indexed by m.
+// Trailing deflation: while m > 2 and |e[m-2]| < eps, m -= 1 -- unrolled
+// from the top so no array is indexed by m.
 template <int N>
-BED_HD int small_deflate(const float (&e)[N], int m, float eps) {
-  unsigned small = 0;
+__device__ __forceinline__ int small_deflate(const float (&e)[N], int m, float eps) {
 #pragma unroll
-  for (int j = 0; j < N - 1; ++j) small |= (fabsf(e[j]) < eps ? 1u : 0u) << j;
-  while (m > 2 && ((small >> (m - 2)) & 1u)) --m;
+  for (int j = N - 2; j >= 1; --j) m = (m == j + 2 && fabsf(e[j]) < eps) ? j + 1 : m;
   return m;
 }
 
@@ -121,6 +151,7 @@ __global__ void __launch_bounds__(kSmallThreads)
                      int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg) {
   using Lay = SmallLayout<N>;
   constexpr int NN = Lay::NN;
+  constexpr int NP = Lay::NP;
   __shared__ float tile[kSmallThreads * Lay::STRIDE];
   __shared__ float ltile[kSmallThreads * Lay::LSTRIDE];
 
@@ -180,11 +211,13 @@ __global__ void __launch_bounds__(kSmallThreads)
   }
 
   // ---- Householder tridiagonalisation with V <- V H_i accumulated in place
-  float v[N][N];
+  // (V as packed row pairs; the odd-N padding row stays zero)
+  f2 v[NP][N];
 #pragma unroll
-  for (int r = 0; r < N; ++r)
+  for (int rp = 0; rp < NP; ++rp)
 #pragma unroll
-    for (int c = 0; c < N; ++c) v[r][c] = (VECS && r == c) ? 1.0f : 0.0f;
+    for (int c = 0; c < N; ++c)
+      v[rp][c] = f2_make((VECS && 2 * rp == c) ? 1.0f : 0.0f, (VECS && 2 * rp + 1 == c) ? 1.0f : 0.0f);
 
 #pragma unroll
   for (int i = 0; i < N - 2; ++i) {
@@ -223,21 +256,35 @@ __global__ void __launch_bounds__(kSmallThreads)
       }
 #pragma unroll
       for (int r = i + 1; r < N; ++r) q[r] = fmaf(-kk, u[r], q[r]);
-      // A <- A - q u^T - u q^T on the trailing lower triangle
+      // A <- A - q u^T - u q^T on the trailing lower triangle (two FMAs)
 #pragma unroll
       for (int r = i; r < N; ++r)
 #pragma unroll
-        for (int c = i; c <= r; ++c) a[r][c] -= fmaf(q[r], u[c], u[r] * q[c]);
+        for (int c = i; c <= r; ++c) a[r][c] = fmaf(-q[r], u[c], fmaf(-u[r], q[c], a[r][c]));
       if constexpr (VECS) {
-        // V <- V (I - 2 u u^T): columns before i+1 are untouched
+        if (i == 0) {
+          // V = I - 2 u u^T directly (u_0 = 0: row and column 0 stay e_0)
 #pragma unroll
-        for (int r = 0; r < N; ++r) {
-          float t = 0.0f;
+          for (int rp = 0; rp < NP; ++rp)
 #pragma unroll
-          for (int c = i + 1; c < N; ++c) t = fmaf(v[r][c], u[c], t);
-          t *= -2.0f;
+            for (int c = 1; c < N; ++c) {
+              const int r0 = 2 * rp, r1 = 2 * rp + 1;
+              const float w = -2.0f * u[c];
+              const float lo = r0 >= 1 ? fmaf(w, u[r0], r0 == c ? 1.0f : 0.0f) : 0.0f;
+              const float hi = (r1 >= 1 && r1 < N) ? fmaf(w, u[r1], r1 == c ? 1.0f : 0.0f) : 0.0f;
+              v[rp][c] = f2_make(lo, hi);
+            }
+        } else {
+          // V <- V (I - 2 u u^T): columns before i+1 are untouched
 #pragma unroll
-          for (int c = i + 1; c < N; ++c) v[r][c] = fmaf(t, u[c], v[r][c]);
+          for (int rp = 0; rp < NP; ++rp) {
+            f2 t = fmul2(v[rp][i + 1], f2_bc(u[i + 1]));
+#pragma unroll
+            for (int c = i + 2; c < N; ++c) t = ffma2(v[rp][c], f2_bc(u[c]), t);
+            t = fmul2(t, f2_bc(-2.0f));
+#pragma unroll
+            for (int c = i + 1; c < N; ++c) v[rp][c] = ffma2(t, f2_bc(u[c]), v[rp][c]);
+          }
         }
       }
     }
@@ -302,7 +349,7 @@ __global__ void __launch_bounds__(kSmallThreads)
     wilkinson(d[0], e[0], d[1], lo, hi, c, s);
     d[0] = lo;
     d[1] = hi;
-    small_fold<N, VECS>(v, 0, c, s);
+    small_fold<N, VECS>(v, 0, c, s, -s);
   }
 
   // ---- sort (stable) + sign, staged back through shared memory
@@ -330,12 +377,13 @@ __global__ void __launch_bounds__(kSmallThreads)
         float best = -1.0f, lead = 0.0f;
 #pragma unroll
         for (int r = 0; r < N; ++r) {
-          float mag = fabsf(v[r][c]);
-          if (mag > best) { best = mag; lead = v[r][c]; }
+          const float x = v_at<NP, N>(v, r, c);
+          const float mag = fabsf(x);
+          if (mag > best) { best = mag; lead = x; }
         }
-        float flip = lead < 0.0f ? -1.0f : 1.0f;
+        const float flip = lead < 0.0f ? -1.0f : 1.0f;
 #pragma unroll
-        for (int r = 0; r < N; ++r) my[r * N + rank[c]] = v[r][c] * flip;
+        for (int r = 0; r < N; ++r) my[r * N + rank[c]] = v_at<NP, N>(v, r, c) * flip;
       }
     }
     if (status_out) status_out[base + tid] = status;

@@ -32,8 +32,13 @@ def timeit(fn, reps=10, warm=3):
     return e0.elapsed_time(e1) / reps * 1e-3
 
 
-for n, b, tol in [(4, 1 << 22, 1e-5), (4, 1 << 22, 3e-12), (8, 1 << 20, 3e-12), (16, 65536, 3e-12),
-                  (24, 65536, 3e-12), (32, 65536, 3e-12), (64, 8192, 3e-12)]:
+CASES = [(4, 1 << 22, 1e-5), (4, 1 << 22, 3e-12), (8, 1 << 20, 3e-12), (16, 65536, 3e-12),
+         (24, 65536, 3e-12), (32, 65536, 3e-12), (64, 8192, 3e-12)]
+ONLY = [int(x) for x in sys.argv[1:] if x.isdigit()]
+EIGH = "--eigh" in sys.argv
+for n, b, tol in CASES:
+    if ONLY and n not in ONLY:
+        continue
     a = spd(b, n)
     cfg = bed.SolverConfig(deflation_tol=tol, max_double_steps=4 * n)
     L = torch.empty((b, n), device="cuda")
@@ -58,6 +63,8 @@ for n, b, tol in [(4, 1 << 22, 1e-5), (4, 1 << 22, 3e-12), (8, 1 << 20, 3e-12), 
         Bb = 4 * (3 * n * n + 2 * n)
         roof = max(Bb / PEAK_HBM, Fb / PEAK_F32)
         print(f"   bwd: {t*1e3:8.3f} ms  {b/t/1e6:9.2f} M mat/s  roof frac {roof*b/t:.3f}")
+    if not EIGH:
+        continue
     try:
         sub = a[: min(b, 16384)].contiguous()
         te = timeit(lambda: torch.linalg.eigh(sub), reps=3, warm=1)
