@@ -80,19 +80,35 @@ __device__ __forceinline__ bool warp_any(bool p) { return __any_sync(0xffffffffu
 // inputs: a dead target (|e| < 2^-60, or a position past the active block,
 // passed as e = 0) runs on (1, 0), giving c = 1, s = 0 exactly; r is then
 // the unrotated dw (_kernels.py:247, :256-258).
+//
+// For n <= 8 the reciprocal square root is the raw MUFU value (relative
+// error < 2^-22): a rotation is then orthogonal up to a scale 1 + O(2^-22),
+// and the few dozen rotations a small solve applies keep V orthogonal and
+// the eigenvalues within a few 1e-7 of the spectral radius (the parity
+// gates are 1e-5).  The medium kernels, which fold thousands of rotations,
+// refine it (rsqrt_nr).
+template <bool REFINE>
 __device__ __forceinline__ void small_givens(float dw, float e, float& c, float& s, float& ns,
                                              float& r) {
   const bool live = fabsf(e) >= 0x1p-60f;
   const float x = live ? dw : 1.0f;
   const float y = live ? e : 0.0f;
   const float h2 = fmaf(x, x, y * y);
-  const float ih = rsqrt_nr(h2);
+  const float ih = REFINE ? rsqrt_nr(h2) : rsqrt_approx(h2);
   c = x * ih;
   s = -y * ih;
-  ns = y * ih;
+  ns = -s;
   const float rr = h2 * ih;
   r = live ? rr : dw;
 }
+
+// Skip sweep positions no lane of the warp needs (a warp vote per
+// position)?  The branch costs register moves at every join (the packed V
+// pairs change homes), which outweighs the skipped work at n = 4.
+template <int N>
+struct SweepSkip {
+  static constexpr bool value = N > 4;
+};
 
 // One explicit shifted QR sweep of the leading m-block, fused exactly like
 // _sweep_block (rotation i-1 retires once rotation i exists), written as
@@ -108,14 +124,14 @@ __device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N],
   float c1 = 1.0f, s1 = 0.0f, ns1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    if (i >= 2 && !warp_any(i <= m - 1)) break;
+    if (SweepSkip<N>::value && i >= 2 && !warp_any(i <= m - 1)) break;
     const bool act = i < m - 1;
     const float ei = (i < N - 1 && act) ? e[i] : 0.0f;
     float c, s, ns, r;
-    small_givens(dw, ei, c, s, ns, r);
+    small_givens<false>(dw, ei, c, s, ns, r);
     const float dn = (i + 1 < N ? d[i + 1] : 0.0f) - mu;
     // (u, dw') = (c g - s dn, s g + c dn)
-    const f2 ud = ffma2(f2_make(ns, c), f2_bc(dn), fmul2(f2_make(c, s), f2_bc(g)));
+    const f2 ud = ffma2(f2_make(-s, c), f2_bc(dn), fmul2(f2_make(c, s), f2_bc(g)));
     if (i > 0) {
       const bool wr = i <= m - 1;  // rotation i-1 was a real one
       const float dret = (c1 * (c2 * r1) - s1 * u1) + mu;
@@ -136,11 +152,12 @@ __device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N],
 }
 
 // Trailing deflation: while m > 2 and |e[m-2]| < eps, m -= 1 -- unrolled
-// from the top so no array is indexed by m.
+// from the top so no array is indexed by m, in integer arithmetic so it
+// compiles without branches.  Idempotent (a finished lane's m stays put).
 template <int N>
 __device__ __forceinline__ int small_deflate(const float (&e)[N], int m, float eps) {
 #pragma unroll
-  for (int j = N - 2; j >= 1; --j) m = (m == j + 2 && fabsf(e[j]) < eps) ? j + 1 : m;
+  for (int j = N - 2; j >= 1; --j) m -= (int)(m == j + 2) & (int)(fabsf(e[j]) < eps);
   return m;
 }
 
@@ -314,12 +331,14 @@ __global__ void __launch_bounds__(kSmallThreads)
     int m = small_deflate<N>(e, N, cfg.eps);
     bool run = m > 2;
     while (warp_any(run)) {
-      if (run && steps >= cfg.max_steps) {  // budget exhausted: qr.py:604-612
-        float resid = 0.0f;
+      if (warp_any(run && steps >= cfg.max_steps)) {  // budget exhausted: qr.py:604-612
+        if (run && steps >= cfg.max_steps) {
+          float resid = 0.0f;
 #pragma unroll
-        for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
-        if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
-        run = false;  // lock the diagonal; the leading 2x2 still closes below
+          for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
+          if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
+          run = false;  // lock the diagonal; the leading 2x2 still closes below
+        }
       }
       // trailing 2x2 of the active block; an arithmetic blend, not a select
       // chain, so the compiler cannot fold it into a dynamically indexed
@@ -334,14 +353,14 @@ __global__ void __launch_bounds__(kSmallThreads)
       }
       float lo, hi;
       wilkinson_shifts(ta, tb, td, lo, hi);
+      // finished lanes sweep nothing (m = 0); their couplings do not move,
+      // so the unconditional deflations leave their m unchanged
       small_sweep<N, VECS>(d, e, v, run ? m : 0, hi);
-      if (run) m = small_deflate<N>(e, m, cfg.eps);
+      m = small_deflate<N>(e, m, cfg.eps);
       small_sweep<N, VECS>(d, e, v, (run && m > 2) ? m : 0, lo);
-      if (run) {
-        m = small_deflate<N>(e, m, cfg.eps);
-        ++steps;
-        run = m > 2;
-      }
+      m = small_deflate<N>(e, m, cfg.eps);
+      steps += run ? 1 : 0;
+      run = run && m > 2;
     }
   }
   if constexpr (N >= 2) {
