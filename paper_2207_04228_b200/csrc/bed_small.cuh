@@ -102,9 +102,11 @@ __device__ __forceinline__ void small_givens(float dw, float e, float& c, float&
   r = live ? rr : dw;
 }
 
-// Skip sweep positions no lane of the warp needs (a warp vote per
-// position)?  The branch costs register moves at every join (the packed V
-// pairs change homes), which outweighs the skipped work at n = 4.
+// How sweeps avoid positions no lane of the warp needs.  n > 4: a warp vote
+// per position.  n <= 4: that branch costs register moves at every join (the
+// packed V pairs change homes), so the QR loop is instead compiled once per
+// warp-maximum active size MA = n, n-1, ..., 3, each copy sweeping exactly
+// MA positions; a warp moves to the next copy when no lane has m == MA.
 template <int N>
 struct SweepSkip {
   static constexpr bool value = N > 4;
@@ -115,15 +117,14 @@ struct SweepSkip {
 // predicated straight-line code: rotations at positions >= m-1 degenerate to
 // the identity and writes past the active block are masked with selects.
 // m = 0 makes the whole sweep a no-op (used for lanes whose matrix has
-// finished).  Position i is skipped outright when no lane of the warp needs
-// it.
-template <int N, bool VECS>
+// finished).  Only positions below MA (>= every lane's m) are processed.
+template <int N, bool VECS, int MA = N>
 __device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N],
                                             f2 (&v)[SmallLayout<N>::NP][N], int m, float mu) {
   float dw = d[0] - mu, g = e[0];
   float c1 = 1.0f, s1 = 0.0f, ns1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
+  for (int i = 0; i < MA; ++i) {
     if (SweepSkip<N>::value && i >= 2 && !warp_any(i <= m - 1)) break;
     const bool act = i < m - 1;
     const float ei = (i < N - 1 && act) ? e[i] : 0.0f;
@@ -330,37 +331,40 @@ __global__ void __launch_bounds__(kSmallThreads)
   if constexpr (N >= 3) {
     int m = small_deflate<N>(e, N, cfg.eps);
     bool run = m > 2;
-    while (warp_any(run)) {
-      if (warp_any(run && steps >= cfg.max_steps)) {  // budget exhausted: qr.py:604-612
-        if (run && steps >= cfg.max_steps) {
-          float resid = 0.0f;
+    auto phase = [&](auto mac) {
+      constexpr int MA = decltype(mac)::value;
+      while (warp_any(run) && (MA == 3 || SweepSkip<N>::value || warp_any(m == MA))) {
+        if (warp_any(run && steps >= cfg.max_steps)) {  // budget exhausted: qr.py:604-612
+          if (run && steps >= cfg.max_steps) {
+            float resid = 0.0f;
 #pragma unroll
-          for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
-          if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
-          run = false;  // lock the diagonal; the leading 2x2 still closes below
+            for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
+            if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
+            run = false;  // lock the diagonal; the leading 2x2 still closes below
+          }
         }
-      }
-      // trailing 2x2 of the active block; an arithmetic blend, not a select
-      // chain, so the compiler cannot fold it into a dynamically indexed
-      // (local-memory) load of d[m-2]
-      float ta = 0.0f, tb = 0.0f, td = 0.0f;
+        float ta = 0.0f, tb = 0.0f, td = 0.0f;
 #pragma unroll
-      for (int j = 1; j < N - 1; ++j) {
-        const float w = (j == m - 2) ? 1.0f : 0.0f;
-        ta = fmaf(w, d[j], ta);
-        tb = fmaf(w, e[j], tb);
-        td = fmaf(w, d[j + 1], td);
+        for (int j = 1; j < MA - 1; ++j) {
+          const float w = (j == m - 2) ? 1.0f : 0.0f;
+          ta = fmaf(w, d[j], ta);
+          tb = fmaf(w, e[j], tb);
+          td = fmaf(w, d[j + 1], td);
+        }
+        float lo, hi;
+        wilkinson_shifts(ta, tb, td, lo, hi);
+        small_sweep<N, VECS, MA>(d, e, v, run ? m : 0, hi);
+        m = small_deflate<N>(e, m, cfg.eps);
+        small_sweep<N, VECS, MA>(d, e, v, (run && m > 2) ? m : 0, lo);
+        m = small_deflate<N>(e, m, cfg.eps);
+        steps += run ? 1 : 0;
+        run = run && m > 2;
       }
-      float lo, hi;
-      wilkinson_shifts(ta, tb, td, lo, hi);
-      // finished lanes sweep nothing (m = 0); their couplings do not move,
-      // so the unconditional deflations leave their m unchanged
-      small_sweep<N, VECS>(d, e, v, run ? m : 0, hi);
-      m = small_deflate<N>(e, m, cfg.eps);
-      small_sweep<N, VECS>(d, e, v, (run && m > 2) ? m : 0, lo);
-      m = small_deflate<N>(e, m, cfg.eps);
-      steps += run ? 1 : 0;
-      run = run && m > 2;
+    };
+    if constexpr (SweepSkip<N>::value) {
+      phase(std::integral_constant<int, N>{});
+    } else {
+      static_for<0, N - 2>([&](auto kc) { phase(std::integral_constant<int, N - decltype(kc)::value>{}); });
     }
   }
   if constexpr (N >= 2) {
