@@ -178,39 +178,47 @@ __global__ void __launch_bounds__(kSmallThreads)
   const int tid = threadIdx.x;
   const bool live = tid < count;
 
-  // ---- coalesced tile load (128-bit when the tile is 16-byte aligned)
-  {
-    const float* src = A + base * NN;
-    const int total = count * NN;
-    if ((NN % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-      const float4* src4 = reinterpret_cast<const float4*>(src);
-      for (int g4 = tid; g4 < total / 4; g4 += kSmallThreads) {
-        float4 x = __ldg(src4 + g4);
-        int g = 4 * g4;
-        int mat = g / NN, off = g % NN;
-        float* dst = tile + mat * Lay::STRIDE + off;  // NN%4==0: no row straddle
-        dst[0] = x.x; dst[1] = x.y; dst[2] = x.z; dst[3] = x.w;
-      }
-    } else {
-      for (int g = tid; g < total; g += kSmallThreads)
-        tile[(g / NN) * Lay::STRIDE + (g % NN)] = __ldg(src + g);
-    }
-  }
-  __syncthreads();
-
-  // ---- validate + symmetrise (core.py:286-309)
+  // ---- load.  n^2 % 4 == 0 with a 16-byte aligned batch: each thread reads
+  // its own matrix with 128-bit loads (the warp's n^2/4 loads cover one
+  // contiguous span; L1 merges the sectors).  Otherwise a coalesced tile
+  // load into the odd-stride shared stage.  The branch is CTA-uniform.
   float a[N][N];
   int status = kStatusOk;
   {
-    const float* my = tile + tid * Lay::STRIDE;
     float x[N][N];
+    const bool direct = (NN % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    if (direct) {
+      if constexpr (NN % 4 == 0) {
+        const float4* p = reinterpret_cast<const float4*>(A + (base + (live ? tid : 0)) * NN);
+#pragma unroll
+        for (int q = 0; q < NN / 4; ++q) {
+          float4 t = __ldg(p + q);
+          if (!live) t = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          x[(4 * q) / N][(4 * q) % N] = t.x;
+          x[(4 * q + 1) / N][(4 * q + 1) % N] = t.y;
+          x[(4 * q + 2) / N][(4 * q + 2) % N] = t.z;
+          x[(4 * q + 3) / N][(4 * q + 3) % N] = t.w;
+        }
+      }
+    } else {
+      const float* src = A + base * NN;
+      for (int g = tid; g < count * NN; g += kSmallThreads)
+        tile[(g / NN) * Lay::STRIDE + (g % NN)] = __ldg(src + g);
+      __syncthreads();
+      const float* my = tile + tid * Lay::STRIDE;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) x[r][c] = live ? my[r * N + c] : 0.0f;
+    }
+
+    // ---- validate + symmetrise (core.py:286-309)
     bool finite = true;
     float fro2 = 0.0f, asym = 0.0f;
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        x[r][c] = live ? my[r * N + c] : 0.0f;
         finite = finite && isfinite(x[r][c]);
         fro2 = fmaf(x[r][c], x[r][c], fro2);
       }
@@ -375,18 +383,23 @@ __global__ void __launch_bounds__(kSmallThreads)
     small_fold<N, VECS>(v, 0, c, s, -s);
   }
 
-  // ---- sort (stable) + sign, staged back through shared memory
+  // ---- sort (stable) + sign, staged back through shared memory.  Ranks
+  // from one comparison per pair: with x = d (descending) or -d
+  // (ascending), k < c sorts first iff x_k >= x_c (ties keep index order,
+  // solver.py:60-76).
   int rank[N];
 #pragma unroll
-  for (int c = 0; c < N; ++c) {
-    int rk = 0;
-    if (cfg.sort != 0) {
+  for (int c = 0; c < N; ++c) rank[c] = cfg.sort != 0 ? 0 : c;
+  if (cfg.sort != 0) {
+    const float sg = cfg.sort == 1 ? 1.0f : -1.0f;
 #pragma unroll
-      for (int k = 0; k < N; ++k) rk += (k != c && rank_before(d[k], k, d[c], c, cfg.sort)) ? 1 : 0;
-    } else {
-      rk = c;
-    }
-    rank[c] = rk;
+    for (int c = 1; c < N; ++c)
+#pragma unroll
+      for (int k = 0; k < c; ++k) {
+        const int kb = (sg * d[k] >= sg * d[c]) ? 1 : 0;
+        rank[c] += kb;
+        rank[k] += 1 - kb;
+      }
   }
   __syncthreads();  // every thread is done reading its input tile
   if (live) {
