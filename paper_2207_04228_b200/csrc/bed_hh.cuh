@@ -1,0 +1,315 @@
+// bed_hh.cuh -- H stage of the medium path (9 <= n <= 64): validation,
+// Householder tridiagonalisation and P = H_0 H_1 ... H_{n-3}.
+//
+// One warp (NMAX = 32, 64) or half-warp (NMAX = 16) owns a matrix; lane l
+// holds rows l and, for NMAX = 64, l + 32 of A in registers as packed column
+// pairs (bed_f32x2.cuh), so every p = A u product and every symmetric rank-2
+// update runs as FFMA2 on two columns at once, with the reflector u and the
+// vector q read back from shared memory as 128-bit broadcasts.  All group
+// communication is warp shuffles -- no named barriers, no shared-memory
+// reductions -- so a CTA holds several independent matrices and the SM
+// keeps 8-16 of them in flight.
+//
+// Reference (/root/reference/pkg/src/batchedeig):
+//   validate + symmetrise      core.py:286-309
+//   reflector                  householder.py:97-118 / _kernels.py:47-68
+//   rank-2 update              householder.py:121-126 / _kernels.py:70-92
+//   band                       householder.py:207-213
+//   P (accumulate reflectors)  householder.py:216-231
+//
+// The reference scales every reflector's tail by its max |.| before the
+// norm (householder.py:97-118), which guards float64 over/underflow.  Here
+// the whole matrix is scaled once by the power of two 2^-ceil(log2 max|a|)
+// (exact; Householder steps preserve the Frobenius norm, so every tail then
+// has |x| <= n and its square sum cannot overflow), and the band is scaled
+// back exactly.  Tails whose square sum underflows (below ~1e-19 of the
+// matrix norm) count as already reduced -- the reference's zero-tail rule
+// (householder.py:37-39) at FP32 resolution.
+#pragma once
+
+#include "bed_f32x2.cuh"
+#include "bed_split_ws.cuh"
+#include "bed_tile.cuh"
+
+namespace bed {
+
+template <int NMAX>
+struct HHParams {
+  static constexpr int L = NMAX <= 16 ? 16 : 32;  // lanes per matrix
+  static constexpr int R = (NMAX + 31) / 32;       // rows per lane
+  static constexpr int MINB = NMAX == 64 ? 1 : (NMAX <= 16 ? 4 : 3);  // CTAs per SM the register cap must allow
+  static constexpr int NP = NMAX / 2;              // column pairs per row
+  static constexpr int G = NMAX == 64 ? 4 : 256 / L;  // matrices per CTA
+  static constexpr int THREADS = G * L;
+  static constexpr int SROW = NMAX + 4;            // 16-byte rows, conflict-free row reads
+  static constexpr int SMAT = NMAX * SROW + NMAX;  // stage / reflectors + q
+  static constexpr size_t BYTES = sizeof(float) * (size_t)G * SMAT;
+};
+
+template <int L>
+__device__ __forceinline__ float group_sum(float x, unsigned mask) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o, L);
+  return x;
+}
+template <int L>
+__device__ __forceinline__ float group_max(float x, unsigned mask) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(mask, x, o, L));
+  return x;
+}
+
+// component c of a packed row (c a compile-time constant at every call)
+template <int NP>
+__device__ __forceinline__ float col_of(const f2 (&row)[NP], int c) {
+  return (c & 1) ? f2_hi(row[c >> 1]) : f2_lo(row[c >> 1]);
+}
+
+template <int NMAX, bool EXACT, bool VECS>
+__global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
+    bed_hh_kernel(const float* __restrict__ A, int64_t bc, int n_rt, SplitWs ws, KernelCfg cfg) {
+  using P = HHParams<NMAX>;
+  constexpr int L = P::L, R = P::R, NP = P::NP, G = P::G, SROW = P::SROW;
+  const int n = EXACT ? NMAX : n_rt;
+  const int nn = n * n;
+  extern __shared__ __align__(16) float smem[];
+  const int tid = threadIdx.x;
+  const int mi = tid / L;
+  const int l = tid % L;
+  const unsigned mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
+  const int64_t j0 = (int64_t)blockIdx.x * G;
+  const int count = (bc - j0) < G ? (int)(bc - j0) : G;
+  const bool mlive = mi < count;
+  const int64_t j = j0 + mi;
+  float* st = smem + mi * P::SMAT;  // rows of A, later reflector rows, later P rows
+  float* qv = st + NMAX * SROW;     // q of the current step
+
+  {  // coalesced tile load into the 16-byte-row stage (padding zero-filled)
+    if (!EXACT) {
+      for (int g = tid; g < G * P::SMAT; g += P::THREADS) smem[g] = 0.0f;
+      __syncthreads();
+    }
+    tile_to_stage<NMAX, P::THREADS, SROW, P::SMAT>(A + j0 * nn, count, n, smem);
+  }
+  __syncthreads();
+
+  // ---- validate + symmetrise (core.py:286-309); rows via 128-bit reads,
+  // the transposed entries via conflict-free column reads
+  f2 a[R][NP];
+  int status = kStatusOk;
+  float prescale = 1.0f, unscale = 1.0f;
+  {
+    bool finite = true;
+    float amax = 0.0f, asym = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int row = l + 32 * rr;
+      const bool ok = mlive && row < NMAX;  // NMAX = 24: lanes 24..31 hold no row
+      const float4* r4 = reinterpret_cast<const float4*>(st + (ok ? row : 0) * SROW);
+#pragma unroll
+      for (int k4 = 0; k4 < NMAX / 4; ++k4) {
+        const float4 x = ok ? r4[k4] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+        float ys[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          ys[t] = ok ? st[(4 * k4 + t) * SROW + row] : 0.0f;
+          finite = finite && isfinite(xs[t]);
+          amax = fmaxf(amax, fabsf(xs[t]));
+          asym = fmaxf(asym, fabsf(xs[t] - ys[t]));
+        }
+        a[rr][2 * k4] = f2_make(0.5f * (xs[0] + ys[0]), 0.5f * (xs[1] + ys[1]));
+        a[rr][2 * k4 + 1] = f2_make(0.5f * (xs[2] + ys[2]), 0.5f * (xs[3] + ys[3]));
+      }
+    }
+    finite = group_max<L>(finite ? 0.0f : 1.0f, mask) == 0.0f;
+    amax = group_max<L>(amax, mask);
+    asym = group_max<L>(asym, mask);
+    prescale = 1.0f;
+    if (finite) unscale = pow2_ceil(amax, &prescale);
+    // ||A||_F of the prescaled matrix (entries <= 1: no overflow)
+    float fro2 = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const f2 y = fmul2(a[rr][k], f2_bc(prescale));
+        fro2 = fmaf(f2_lo(y), f2_lo(y), fmaf(f2_hi(y), f2_hi(y), fro2));
+      }
+    fro2 = group_sum<L>(fro2, mask);
+    if (!finite) {
+      status = kStatusNonFinite;
+    } else if (asym > cfg.sym_tol * fmaxf(1.0f, sqrtf(fro2) * unscale)) {
+      status = kStatusNonSym;
+    }
+    const float f = status == kStatusOk ? prescale : 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) a[rr][k] = fmul2(a[rr][k], f2_bc(f));
+  }
+  __syncwarp(mask);  // stage rows are about to be reused for reflectors
+
+  // ---- Householder reduction; reflector i stored in st row i.  The step
+  // loop is expanded by template recursion so every column index is a
+  // compile-time constant (NVVM's unroller gives up on the n = 64 body).
+  static_for<0, NMAX - 2>([&](auto ic) {
+    constexpr int i = decltype(ic)::value;
+    if (!EXACT && i >= n - 2) return;
+    float x[R];
+    float ss = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      x[rr] = (l + 32 * rr > i) ? col_of<NP>(a[rr], i) : 0.0f;
+      ss = fmaf(x[rr], x[rr], ss);
+    }
+    ss = group_sum<L>(ss, mask);
+    float* urow = st + i * SROW;
+    float u[R];
+    if (ss > 0x1p-120f) {
+      // sigma = sign(x_0) ||x||, u0 = x_0 + sigma, ||u||^2 = 2 sigma u0
+      // (householder.py:97-118; the tail is already at unit scale)
+      constexpr int pr = (i + 1) / 32, pl = (i + 1) % 32;
+      const float pivot = __shfl_sync(mask, x[pr], pl, L);
+      const float nrm = ss * rsqrt_nr(ss);
+      const float sigma = pivot >= 0.0f ? nrm : -nrm;
+      const float u0 = pivot + sigma;
+      const float iu = rsqrt_nr(2.0f * sigma * u0);  // sigma, u0 share a sign
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        u[rr] = (l + 32 * rr == i + 1 ? u0 : x[rr]) * iu;  // x = 0 for rows <= i
+        if (l + 32 * rr < NMAX) urow[l + 32 * rr] = u[rr];
+      }
+      __syncwarp(mask);
+      // p = 2 A u (two accumulators per row for ILP), K = u^T p, q = p - K u
+      constexpr int k0 = ((i + 1) / 2) & ~1;  // 16-byte aligned start; u = 0 below i+1
+      float p[R];
+      float kk = 0.0f;
+      {
+        f2 acc0[R], acc1[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = f2_bc(0.0f);
+#pragma unroll
+        for (int k = k0; k < NP; k += 2) {
+          const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            acc0[rr] = ffma2(a[rr][k], f2_make(u4.x, u4.y), acc0[rr]);
+            if (k + 1 < NP) acc1[rr] = ffma2(a[rr][k + 1], f2_make(u4.z, u4.w), acc1[rr]);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const f2 acc = fadd2(acc0[rr], acc1[rr]);
+          p[rr] = 2.0f * (f2_lo(acc) + f2_hi(acc));
+          kk = fmaf(u[rr], p[rr], kk);
+        }
+      }
+      kk = group_sum<L>(kk, mask);
+      float q[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        q[rr] = (l + 32 * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
+        if (l + 32 * rr < NMAX) qv[l + 32 * rr] = q[rr];
+      }
+      __syncwarp(mask);
+      // A <- A - q u^T - u q^T on columns >= i (u, q vanish on the rest)
+      constexpr int k1 = (i / 2) & ~1;
+#pragma unroll
+      for (int k = k1; k < NP; k += 2) {
+        const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
+        const float4 q4 = *reinterpret_cast<const float4*>(qv + 2 * k);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          a[rr][k] = ffma2(f2_bc(-u[rr]), f2_make(q4.x, q4.y),
+                           ffma2(f2_bc(-q[rr]), f2_make(u4.x, u4.y), a[rr][k]));
+          if (k + 1 < NP)
+            a[rr][k + 1] = ffma2(f2_bc(-u[rr]), f2_make(q4.z, q4.w),
+                                 ffma2(f2_bc(-q[rr]), f2_make(u4.z, u4.w), a[rr][k + 1]));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        if (l + 32 * rr < NMAX) urow[l + 32 * rr] = 0.0f;
+    }
+    __syncwarp(mask);
+  });
+
+  // ---- band: D[r] = a(r, r), E[r-1] = a(r, r-1), picked with compares on
+  // the lane index so no register array is indexed at run time
+  if (mlive) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int row = l + 32 * rr;
+      float dv = 0.0f, ev = 0.0f;
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c) {
+        const float x = col_of<NP>(a[rr], c);
+        dv = row == c ? x : dv;
+        ev = row == c + 1 ? x : ev;
+      }
+      if (row < n) ws.D[(int64_t)row * ws.Bc + j] = dv * unscale;
+      if (row >= 1 && row < n) ws.E[(int64_t)(row - 1) * ws.Bc + j] = ev * unscale;
+    }
+    if (l == 0) ws.vstat[j] = status;
+  }
+
+  if constexpr (VECS) {
+    // ---- P = H_0 H_1 ... (householder.py:216-231), rows in registers:
+    // V <- V (I - 2 u u^T) touches columns > i only
+    f2 v[R][NP];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        v[rr][k] = f2_make(l + 32 * rr == 2 * k ? 1.0f : 0.0f, l + 32 * rr == 2 * k + 1 ? 1.0f : 0.0f);
+    static_for<0, NMAX - 2>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if (!EXACT && i >= n - 2) return;
+      const float* urow = st + i * SROW;
+      constexpr int k0 = ((i + 1) / 2) & ~1;
+      f2 acc0[R], acc1[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = f2_bc(0.0f);
+#pragma unroll
+      for (int k = k0; k < NP; k += 2) {
+        const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          acc0[rr] = ffma2(v[rr][k], f2_make(u4.x, u4.y), acc0[rr]);
+          if (k + 1 < NP) acc1[rr] = ffma2(v[rr][k + 1], f2_make(u4.z, u4.w), acc1[rr]);
+        }
+      }
+      float t[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const f2 acc = fadd2(acc0[rr], acc1[rr]);
+        t[rr] = -2.0f * (f2_lo(acc) + f2_hi(acc));
+      }
+#pragma unroll
+      for (int k = k0; k < NP; k += 2) {
+        const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          v[rr][k] = ffma2(f2_bc(t[rr]), f2_make(u4.x, u4.y), v[rr][k]);
+          if (k + 1 < NP) v[rr][k + 1] = ffma2(f2_bc(t[rr]), f2_make(u4.z, u4.w), v[rr][k + 1]);
+        }
+      }
+    });
+    __syncwarp(mask);  // every lane is done reading reflectors
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (l + 32 * rr >= NMAX) continue;
+      float4* r4 = reinterpret_cast<float4*>(st + (l + 32 * rr) * SROW);
+#pragma unroll
+      for (int k4 = 0; k4 < NMAX / 4; ++k4)
+        r4[k4] = make_float4(f2_lo(v[rr][2 * k4]), f2_hi(v[rr][2 * k4]), f2_lo(v[rr][2 * k4 + 1]),
+                             f2_hi(v[rr][2 * k4 + 1]));
+    }
+    __syncthreads();
+    stage_to_tile<NMAX, P::THREADS, SROW, P::SMAT>(smem, count, n, ws.P + j0 * nn);
+  }
+}
+
+}  // namespace bed

@@ -31,185 +31,13 @@
 // the eigenvalues itself.
 #pragma once
 
+#include "bed_f32x2.cuh"
 #include "bed_group.cuh"
+#include "bed_hh.cuh"
+#include "bed_split_ws.cuh"
+#include "bed_tile.cuh"
 
 namespace bed {
-
-constexpr int kFoldBlk = 8;    // positions per static fold block
-constexpr int kQThreads = 128;
-
-struct SplitWs {
-  float* P;         // [bc][n][n] initial V (VECS)
-  float* D;         // [n][Bc] band diagonal, position-major
-  float* E;         // [n][Bc] band off-diagonal
-  float* lam;       // [n][Bc] unsorted eigenvalues (VECS)
-  int32_t* vstat;   // [Bc] validation status from H
-  float2* rot;      // [W][Smax][NMAX-1][32] recorded rotations (VECS)
-  int32_t* msw;     // [W][Smax] warp-maximum active size of each recorded sweep
-  int32_t* nsw;     // [W] sweeps recorded by warp w
-  int64_t Bc;       // chunk capacity (multiple of 32)
-  int Smax;         // sweep records per warp
-};
-
-template <int NMAX>
-struct HHParams {
-  static constexpr int L = GroupSize<NMAX>::L;
-  static constexpr int G = 256 / L;  // matrices per CTA
-  static constexpr int THREADS = G * L;
-  static constexpr int SROW = NMAX + 1;
-  static constexpr int SMAT = NMAX * SROW;
-  static constexpr int OFF_Q = G * SMAT;
-  static constexpr int OFF_RED = OFF_Q + G * NMAX;
-  static constexpr int TOTAL = OFF_RED + 4 * G;
-  static constexpr size_t BYTES = sizeof(float) * TOTAL;
-};
-
-// ---------------------------------------------------------------------------
-// H: validation, Householder reduction, P.
-template <int NMAX, bool EXACT, bool VECS>
-__global__ void __launch_bounds__(HHParams<NMAX>::THREADS, NMAX <= 32 ? 3 : 1)
-    bed_hh_kernel(const float* __restrict__ A, int64_t bc, int n_rt, SplitWs ws, KernelCfg cfg) {
-  using P = HHParams<NMAX>;
-  constexpr int L = P::L, G = P::G;
-  const int n = EXACT ? NMAX : n_rt;
-  const int nn = n * n;
-  extern __shared__ __align__(16) float smem[];
-  const int tid = threadIdx.x;
-  const int mi = tid / L;
-  const int r = tid % L;
-  Group<L> grp;
-  grp.init(tid, mi, smem + P::OFF_RED + 4 * mi);
-  const int64_t j0 = (int64_t)blockIdx.x * G;
-  const int count = (bc - j0) < G ? (int)(bc - j0) : G;
-  const bool mlive = mi < count;
-  const int64_t j = j0 + mi;
-  float* st = smem + mi * P::SMAT;
-  float* qrow = smem + P::OFF_Q + mi * NMAX;
-
-  {  // coalesced tile load into the padded stage
-    const float* src = A + j0 * nn;
-    for (int g = tid; g < count * nn; g += P::THREADS) {
-      int mat = g / nn, off = g - mat * nn;
-      int rr = off / n, c = off - rr * n;
-      smem[mat * P::SMAT + rr * P::SROW + c] = __ldg(src + g);
-    }
-  }
-  __syncthreads();
-
-  float a[NMAX];
-  int status = kStatusOk;
-  {  // validate + symmetrise (core.py:286-309)
-    bool finite = true;
-    float fro2 = 0.0f, asym = 0.0f;
-#pragma unroll
-    for (int c = 0; c < NMAX; ++c) {
-      float x = 0.0f, y = 0.0f;
-      if (mlive && r < n && c < n) {
-        x = st[r * P::SROW + c];
-        y = st[c * P::SROW + r];
-      }
-      finite = finite && isfinite(x);
-      fro2 = fmaf(x, x, fro2);
-      asym = fmaxf(asym, fabsf(x - y));
-      a[c] = 0.5f * (x + y);
-    }
-    finite = grp.max(finite ? 0.0f : 1.0f) == 0.0f;
-    fro2 = grp.sum(fro2);
-    asym = grp.max(asym);
-    if (!finite) status = kStatusNonFinite;
-    else if (asym > cfg.sym_tol * fmaxf(1.0f, sqrtf(fro2))) status = kStatusNonSym;
-    if (status != kStatusOk) {
-#pragma unroll
-      for (int c = 0; c < NMAX; ++c) a[c] = 0.0f;
-    }
-  }
-  grp.sync();  // stage rows are about to be reused for reflectors
-
-  // Householder reduction, reflector i stored in st[i][*].  The step loop is
-  // expanded by template recursion: NVVM's unroller gives up on the n = 64
-  // body and would demote the row to local memory.
-  static_for<0, NMAX - 2>([&](auto ic) {
-    constexpr int i = decltype(ic)::value;
-    if (!EXACT && i >= n - 2) return;
-    const float x = r > i ? a[i] : 0.0f;
-    const float scale = grp.max(fabsf(x));
-    float* urow = st + i * P::SROW;
-    if (scale > kZeroTail) {
-      // reflector of the scaled tail xs = tail/scale (householder.py:97-118):
-      // sigma = sign(xs_0) ||xs||, u0 = xs_0 + sigma, ||u||^2 = 2 sigma u0
-      const float xs = x * rcp_fast(scale);
-      const float ss = grp.sum(xs * xs);
-      const float pivot = grp.bcast(xs, i + 1);
-      const float nrm = ss * rsqrt_nr(ss);
-      const float sigma = pivot >= 0.0f ? nrm : -nrm;
-      const float u0 = pivot + sigma;
-      const float iu = rsqrt_nr(2.0f * sigma * u0);  // sigma, u0 share a sign
-      const float u = (r == i + 1 ? u0 : xs) * iu;   // xs = 0 for r <= i
-      if (r < NMAX) urow[r] = u;
-      grp.sync();
-      // p = 2 A u, K = u^T p, q = p - K u (zero above row i)
-      float p = 0.0f;
-#pragma unroll
-      for (int c = i + 1; c < NMAX; ++c) p = fmaf(a[c], urow[c], p);
-      p *= 2.0f;
-      const float kk = grp.sum(u * p);
-      const float q = r >= i ? fmaf(-kk, u, p) : 0.0f;
-      if (r < NMAX) qrow[r] = q;
-      grp.sync();
-      if (r >= i) {  // A <- A - q u^T - u q^T as two FMAs per entry (u_i = 0)
-        a[i] = fmaf(-u, qrow[i], a[i]);
-#pragma unroll
-        for (int c = i + 1; c < NMAX; ++c) a[c] = fmaf(-q, urow[c], fmaf(-u, qrow[c], a[c]));
-      }
-    } else if (r < NMAX) {
-      urow[r] = 0.0f;
-    }
-    grp.sync();
-  });
-  // band: D[r] = a(r, r), E[r-1] = a(r, r-1), extracted with an arithmetic
-  // blend so no register array is indexed at run time
-  if (mlive) {
-    float dv = 0.0f, ev = 0.0f;
-#pragma unroll
-    for (int c = 0; c < NMAX; ++c) {
-      dv = fmaf(r == c ? 1.0f : 0.0f, a[c], dv);
-      ev = fmaf(r == c + 1 ? 1.0f : 0.0f, a[c], ev);
-    }
-    if (r < n) ws.D[(int64_t)r * ws.Bc + j] = dv;
-    if (r >= 1 && r < n) ws.E[(int64_t)(r - 1) * ws.Bc + j] = ev;
-    if (r == 0) ws.vstat[j] = status;
-  }
-  if constexpr (VECS) {
-    // P = H_0 H_1 ..., row r in registers
-    float v[NMAX];
-#pragma unroll
-    for (int c = 0; c < NMAX; ++c) v[c] = (r == c) ? 1.0f : 0.0f;
-    static_for<0, NMAX - 2>([&](auto ic) {
-      constexpr int i = decltype(ic)::value;
-      if (!EXACT && i >= n - 2) return;
-      const float* urow = st + i * P::SROW;
-      float t = 0.0f;
-#pragma unroll
-      for (int c = i + 1; c < NMAX; ++c) t = fmaf(v[c], urow[c], t);
-      t *= -2.0f;
-#pragma unroll
-      for (int c = i + 1; c < NMAX; ++c) v[c] = fmaf(t, urow[c], v[c]);
-    });
-    grp.sync();  // all reflectors read
-    if (r < n) {
-#pragma unroll
-      for (int c = 0; c < NMAX; ++c)
-        if (c < n) st[r * P::SROW + c] = v[c];
-    }
-    __syncthreads();
-    float* dst = ws.P + j0 * nn;
-    for (int g = tid; g < count * nn; g += P::THREADS) {
-      int mat = g / nn, off = g - mat * nn;
-      int rr = off / n, c = off - rr * n;
-      dst[g] = smem[mat * P::SMAT + rr * P::SROW + c];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Q: one thread per matrix, band in registers, warp-synchronous sweeps.
@@ -297,6 +125,7 @@ __global__ void __launch_bounds__(kQThreads)
 
   float2* recw = VECS ? ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane : nullptr;
   int* mw_rec = VECS ? ws.msw + (size_t)w * ws.Smax : nullptr;
+  uint8_t* ml_rec = VECS ? ws.mlane + (size_t)w * ws.Smax * 32 + lane : nullptr;
   int nrec = 0;
   // pad a recorded sweep with identities up to the fold block boundary
   auto pad = [&](int from, int upto) {
@@ -304,11 +133,14 @@ __global__ void __launch_bounds__(kQThreads)
   };
   // close a record: `written` positions were stored, the fold will run whole
   // blocks up to the one containing position mw - 2
-  auto record_end = [&](int mw, int written) {
+  // blocks up to the one containing position mw - 2; mine is this lane's
+  // active size (the fold skips a lane's no-op sweeps and positions)
+  auto record_end = [&](int mw, int written, int mine) {
     if constexpr (VECS) {
       const int padded = min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk);
       pad(min(written, NMAX - 1), padded);
       if (lane == 0) mw_rec[nrec] = mw;
+      ml_rec[(size_t)nrec * 32] = (uint8_t)mine;
       ++nrec;
     }
   };
@@ -339,13 +171,13 @@ __global__ void __launch_bounds__(kQThreads)
     const int ma = run ? m : 0;
     const int mwa = __reduce_max_sync(0xffffffffu, ma);
     qr_sweep<NMAX, VECS>(d, e, ma, hi, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr);
-    record_end(mwa, mwa);
+    record_end(mwa, mwa, ma);
     if (run) m = qr_deflate<NMAX>(e, m, cfg.eps);
     const int mb = (run && m > 2) ? m : 0;
     const int mwb = __reduce_max_sync(0xffffffffu, mb);
     if (mwb > 2) {
       qr_sweep<NMAX, VECS>(d, e, mb, lo, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr);
-      record_end(mwb, mwb);
+      record_end(mwb, mwb, mb);
     }
     if (run) {
       m = qr_deflate<NMAX>(e, m, cfg.eps);
@@ -360,7 +192,7 @@ __global__ void __launch_bounds__(kQThreads)
     d[1] = hi;
     if constexpr (VECS) {
       recw[(size_t)nrec * (NMAX - 1) * 32] = make_float2(c, s);
-      record_end(2, 1);
+      record_end(2, 1, 2);
     }
   }
   if (VECS && lane == 0) ws.nsw[w] = nrec;
@@ -410,8 +242,10 @@ struct FoldParams {
   static constexpr int SROW = NMAX + 1;
   static constexpr int SMAT = NMAX * SROW;
   static constexpr int PADPOS = ((NMAX - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk;
-  static constexpr int OFF_ROT = G * SMAT;                         // float2 [2][PADPOS][G]
-  static constexpr int OFF_FLIP = OFF_ROT + 2 * 2 * PADPOS * G;
+  static constexpr int RROW = PADPOS + 2;                          // float2 per matrix row
+  static constexpr int OFF_ROT = G * SMAT + (G * SMAT) % 4;        // float2 [2][G][RROW]
+  static constexpr int OFF_MM = OFF_ROT + 2 * 2 * G * RROW;       // int [2][G]
+  static constexpr int OFF_FLIP = OFF_MM + 2 * G;
   static constexpr int OFF_EV = OFF_FLIP + G * NMAX;
   static constexpr int OFF_RANK = OFF_EV + G * NMAX;
   static constexpr int OFF_LAM = OFF_RANK + G * NMAX;
@@ -445,14 +279,7 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
   float* st = smem + mi * P::SMAT;
 
   if (mlive && r < n) lams[mi * NMAX + r] = ws.lam[(int64_t)r * ws.Bc + j];
-  {  // coalesced P tile -> stage
-    const float* src = ws.P + j0 * nn;
-    for (int g = tid; g < count * nn; g += P::THREADS) {
-      int mat = g / nn, off = g - mat * nn;
-      int rr = off / n, c = off - rr * n;
-      smem[mat * P::SMAT + rr * P::SROW + c] = src[g];
-    }
-  }
+  tile_to_stage<NMAX, P::THREADS, P::SROW, P::SMAT>(ws.P + j0 * nn, count, n, smem);
   __syncthreads();
   float v[NMAX];
 #pragma unroll
@@ -464,8 +291,14 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
   const int nrec = ws.nsw[w];
   const int* mws = ws.msw + (size_t)w * ws.Smax;
   const float2* recw = ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane0;
-  // thread t stages elements t, t + THREADS, ... of the [PADPOS][G] block
+  // thread t stages elements t, t + THREADS, ... of the sweep's [PADPOS][G]
+  // block (global order: position-major, lanes contiguous) into the
+  // matrix-major shared buffer [G][RROW], so a group reads two consecutive
+  // rotations with one 128-bit broadcast
+  int* mbuf = reinterpret_cast<int*>(smem + P::OFF_MM);
+  const uint8_t* mls = ws.mlane + (size_t)w * ws.Smax * 32 + lane0;
   float2 pf[P::PER_THREAD];
+  int pm = 0;
   auto fetch = [&](int s2, int npos) {
     const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
 #pragma unroll
@@ -474,13 +307,16 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
       const int p = e / G, g = e - p * G;
       pf[q] = (p < npos) ? __ldg(rs + p * 32 + g) : make_float2(1.0f, 0.0f);
     }
+    if (tid < G) pm = __ldg(mls + (size_t)s2 * 32 + tid);
   };
   auto stash = [&](int buf) {
 #pragma unroll
     for (int q = 0; q < P::PER_THREAD; ++q) {
       const int e = tid + q * P::THREADS;
-      if (e < P::PADPOS * G) rbuf[buf * P::PADPOS * G + e] = pf[q];
+      const int p = e / G, g = e - p * G;
+      if (e < P::PADPOS * G) rbuf[(buf * G + g) * P::RROW + p] = pf[q];
     }
+    if (tid < G) mbuf[buf * G + tid] = pm;
   };
   auto npos_of = [&](int mw) { return min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk); };
   int mw_next = nrec > 0 ? __ldg(mws) : 0;
@@ -492,23 +328,34 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
 #pragma unroll 1
   for (int s2 = 0; s2 < nrec; ++s2) {
     const int buf = s2 & 1;
-    const int mw = mw_next;
     if (s2 + 1 < nrec) {  // prefetch the next sweep while this one is folded
       mw_next = __ldg(mws + s2 + 1);
       fetch(s2 + 1, npos_of(mw_next));
     }
-    if (mlive) {
-      const float2* rs = rbuf + buf * P::PADPOS * G + mi;
+    const int mm = mbuf[buf * G + mi];  // this matrix's active size (0: no-op sweep)
+    if (mlive && mm > 1) {
+      const float2* rs = rbuf + (buf * G + mi) * P::RROW;
       static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bcst) {
         constexpr int b0 = decltype(bcst)::value * kFoldBlk;
         constexpr int b1 = b0 + kFoldBlk < NMAX - 1 ? b0 + kFoldBlk : NMAX - 1;
-        if (b0 < mw - 1) {
+        if (b0 < mm - 1) {
 #pragma unroll
-          for (int p = b0; p < b1; ++p) {
-            const float2 cs = rs[p * G];
-            const float x = v[p], y = v[p + 1];
-            v[p] = cs.x * x - cs.y * y;
-            v[p + 1] = fmaf(cs.y, x, cs.x * y);
+          for (int p = b0; p < b1; p += 2) {
+            // two rotations per 128-bit broadcast; scalar FMAs on purpose:
+            // the packed form (FMUL2 -> FFMA2) lengthens the position-to-
+            // position dependency chain and doubles the row's register
+            // footprint, which measured slower here
+            const float4 c2 = *reinterpret_cast<const float4*>(rs + p);
+            {
+              const float x = v[p], y = v[p + 1];
+              v[p] = c2.x * x - c2.y * y;
+              v[p + 1] = fmaf(c2.y, x, c2.x * y);
+            }
+            if (p + 1 < b1) {
+              const float x = v[p + 1], y = v[p + 2];
+              v[p + 1] = c2.z * x - c2.w * y;
+              v[p + 2] = fmaf(c2.w, x, c2.z * y);
+            }
           }
         }
       });
@@ -549,12 +396,7 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
   }
   __syncthreads();
   {
-    float* dst = evecs + (c0 + j0) * nn;
-    for (int g = tid; g < count * nn; g += P::THREADS) {
-      int mat = g / nn, off = g - mat * nn;
-      int rr = off / n, c = off - rr * n;
-      dst[g] = smem[mat * P::SMAT + rr * P::SROW + c] * flipv[mat * NMAX + c];
-    }
+    stage_to_tile<NMAX, P::THREADS, P::SROW, P::SMAT>(smem, count, n, evecs + (c0 + j0) * nn, flipv);
     float* dstl = evals + (c0 + j0) * n;
     for (int g = tid; g < count * n; g += P::THREADS) {
       int mat = g / n, c = g - mat * n;

@@ -28,7 +28,7 @@ cudaError_t run_split(const FwdArgs& a) {
   const int smax = 2 * a.cfg.max_steps + 1;
   const size_t per = 4 * (2 * (size_t)n) + 4 +
                      (vecs ? 4 * (size_t)nn + 4 * (size_t)n + (size_t)smax * (NMAX - 1) * 8 : 0);
-  const size_t per_warp = vecs ? (size_t)smax * 4 + 4 : 0;
+  const size_t per_warp = vecs ? (size_t)smax * (4 + 32) + 4 : 0;
   const int64_t want = (a.batch + 31) / 32 * 32;
   const size_t need = (size_t)want * (per + per_warp / 32 + 1);
   size_t budget = kSplitWorkspaceBytes;
@@ -54,6 +54,7 @@ cudaError_t run_split(const FwdArgs& a) {
   const size_t oR = vecs ? take((size_t)W * smax * (NMAX - 1) * 32 * 8) : 0;
   const size_t oM = vecs ? take((size_t)W * smax * 4) : 0;
   const size_t oN = vecs ? take((size_t)W * 4) : 0;
+  const size_t oML = vecs ? take((size_t)W * smax * 32) : 0;
   char* base = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), off, a.stream);
   if (e != cudaSuccess) return e;
@@ -66,6 +67,7 @@ cudaError_t run_split(const FwdArgs& a) {
   ws.rot = vecs ? reinterpret_cast<float2*>(base + oR) : nullptr;
   ws.msw = vecs ? reinterpret_cast<int32_t*>(base + oM) : nullptr;
   ws.nsw = vecs ? reinterpret_cast<int32_t*>(base + oN) : nullptr;
+  ws.mlane = vecs ? reinterpret_cast<uint8_t*>(base + oML) : nullptr;
   ws.Bc = Bc;
   ws.Smax = smax;
 

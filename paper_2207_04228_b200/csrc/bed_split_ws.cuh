@@ -1,0 +1,26 @@
+// bed_split_ws.cuh -- workspace shared by the three kernels of the medium
+// path (bed_hh.cuh, bed_split.cuh).
+#pragma once
+
+#include "bed_common.cuh"
+
+namespace bed {
+
+constexpr int kFoldBlk = 8;    // positions per static fold block
+constexpr int kQThreads = 128;
+
+struct SplitWs {
+  float* P;         // [bc][n][n] initial V (VECS)
+  float* D;         // [n][Bc] band diagonal, position-major
+  float* E;         // [n][Bc] band off-diagonal
+  float* lam;       // [n][Bc] unsorted eigenvalues (VECS)
+  int32_t* vstat;   // [Bc] validation status from H
+  float2* rot;      // [W][Smax][NMAX-1][32] recorded rotations (VECS)
+  int32_t* msw;     // [W][Smax] warp-maximum active size of each recorded sweep
+  int32_t* nsw;     // [W] sweeps recorded by warp w
+  uint8_t* mlane;   // [W][Smax][32] each lane's active size in that sweep (0: no-op)
+  int64_t Bc;       // chunk capacity (multiple of 32)
+  int Smax;         // sweep records per warp
+};
+
+}  // namespace bed
