@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -63,6 +64,18 @@ void keep_pool_warm() {
   done[dev] = true;
 }
 
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Bytes of input+output per host-path chunk (env BED_HOST_CHUNK_MB, default 32).
+int64_t host_chunk_bytes() {
+  static int64_t v = [] {
+    const char* e = getenv("BED_HOST_CHUNK_MB");
+    long mb = e ? strtol(e, nullptr, 10) : 0;
+    return (int64_t)(mb > 0 ? mb : 32) << 20;
+  }();
+  return v;
+}
+
 cudaError_t dispatch_forward(const bed::FwdArgs& a) {
   if (a.n > 8) keep_pool_warm();
   if (a.n <= 8) return bed::launch_small(a);
@@ -121,11 +134,13 @@ int bed_backward_f32(const float* V, const float* evals, const float* gV, const 
   return BED_SUCCESS;
 }
 
-// Host-buffer entry: the batch streams through the device in chunks on
-// three rotating streams, so the H2D copy of chunk i+1 and the D2H copy of
-// chunk i-1 overlap the solve of chunk i (copies are only asynchronous when
-// the host buffers are page-locked; pageable buffers still give correct,
-// serialised results).
+// Host-buffer entry: the batch streams through the device in chunks.  Three
+// role streams -- host-to-device copies, solves, device-to-host copies --
+// and a ring of kSlots device buffer sets ordered by events, so the copy
+// engines of both directions run back to back (PCIe is full duplex) while
+// the solves fit in between.  Copies are only asynchronous when the host
+// buffers are page-locked; pageable buffers still give correct, serialised
+// results.
 int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
                          int32_t* status, int32_t* steps, const bed_config* cfg, int32_t device) {
   int rc = check_forward(A, batch, n, evals, evecs, cfg);
@@ -139,57 +154,72 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
 
+  keep_pool_warm();  // the slot buffers come back from the pool on the next call
   const bool vecs = cfg->compute_vectors != 0;
   const int64_t nn = (int64_t)n * n;
   const int64_t per = 4 * (nn + n + (vecs ? nn : 0)) + 8;  // bytes in flight per matrix
-  const int64_t target = 64ll << 20;                         // ~64 MB per chunk
-  const int64_t chunk = std::max<int64_t>(1024, std::min<int64_t>(batch, target / per));
-  constexpr int kStreams = 3;
-  cudaStream_t streams[kStreams] = {};
-  float *dA[kStreams] = {}, *dL[kStreams] = {}, *dV[kStreams] = {};
-  int32_t *dS[kStreams] = {}, *dK[kStreams] = {};
+  const int64_t chunk = std::max<int64_t>(1024, std::min<int64_t>(batch, host_chunk_bytes() / per));
+  constexpr int kSlots = 4;
+  enum { H, C, D };
+  cudaStream_t st[3] = {};
+  cudaEvent_t ev[3][kSlots] = {};
+  char* pool = nullptr;
+  const size_t szA = align_up(sizeof(float) * chunk * nn), szL = align_up(sizeof(float) * chunk * n);
+  const size_t szV = vecs ? align_up(sizeof(float) * chunk * nn) : 0, szI = align_up(sizeof(int32_t) * chunk);
+  const size_t slot = szA + szL + szV + 2 * szI;
   int out = BED_SUCCESS;
-  for (int i = 0; i < kStreams && out == BED_SUCCESS; ++i) {
-    if ((e = cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaMallocAsync(&dA[i], sizeof(float) * chunk * nn, streams[i])) != cudaSuccess ||
-        (e = cudaMallocAsync(&dL[i], sizeof(float) * chunk * n, streams[i])) != cudaSuccess ||
-        (vecs && (e = cudaMallocAsync(&dV[i], sizeof(float) * chunk * nn, streams[i])) != cudaSuccess) ||
-        (e = cudaMallocAsync(&dS[i], sizeof(int32_t) * chunk, streams[i])) != cudaSuccess ||
-        (e = cudaMallocAsync(&dK[i], sizeof(int32_t) * chunk, streams[i])) != cudaSuccess)
-      out = cuda_fail(e, "bed_forward_host_f32 allocation");
+  for (int r = 0; r < 3 && out == BED_SUCCESS; ++r) {
+    if ((e = cudaStreamCreateWithFlags(&st[r], cudaStreamNonBlocking)) != cudaSuccess) out = cuda_fail(e, "stream");
+    for (int b = 0; b < kSlots && out == BED_SUCCESS; ++b)
+      if ((e = cudaEventCreateWithFlags(&ev[r][b], cudaEventDisableTiming)) != cudaSuccess) out = cuda_fail(e, "event");
   }
+  if (out == BED_SUCCESS && (e = cudaMallocAsync(reinterpret_cast<void**>(&pool), slot * kSlots, st[C])) != cudaSuccess)
+    out = cuda_fail(e, "bed_forward_host_f32 allocation");
+  if (out == BED_SUCCESS && (e = cudaEventRecord(ev[C][0], st[C])) == cudaSuccess) {
+    // the H2D stream must not touch the pool before it is allocated
+    e = cudaStreamWaitEvent(st[H], ev[C][0], 0);
+  }
+  if (out == BED_SUCCESS && e != cudaSuccess) out = cuda_fail(e, "event order");
+  bool used[kSlots] = {};
   for (int64_t off = 0, it = 0; off < batch && out == BED_SUCCESS; off += chunk, ++it) {
-    const int i = (int)(it % kStreams);
-    const int64_t b = std::min<int64_t>(chunk, batch - off);
-    cudaStream_t s = streams[i];
-    if ((e = cudaMemcpyAsync(dA[i], A + off * nn, sizeof(float) * b * nn, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
-      out = cuda_fail(e, "H2D");
-      break;
-    }
-    bed::FwdArgs a{dA[i], b, n, dL[i], vecs ? dV[i] : nullptr, dS[i], dK[i], nullptr,
-                   kernel_cfg(cfg, n), s};
-    if ((e = dispatch_forward(a)) != cudaSuccess) {
-      out = cuda_fail(e, "bed_forward_host_f32 launch");
-      break;
-    }
-    if ((e = cudaMemcpyAsync(evals + off * n, dL[i], sizeof(float) * b * n, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-        (vecs && (e = cudaMemcpyAsync(evecs + off * nn, dV[i], sizeof(float) * b * nn, cudaMemcpyDeviceToHost, s)) != cudaSuccess) ||
-        (status && (e = cudaMemcpyAsync(status + off, dS[i], sizeof(int32_t) * b, cudaMemcpyDeviceToHost, s)) != cudaSuccess) ||
-        (steps && (e = cudaMemcpyAsync(steps + off, dK[i], sizeof(int32_t) * b, cudaMemcpyDeviceToHost, s)) != cudaSuccess)) {
-      out = cuda_fail(e, "D2H");
-      break;
-    }
+    const int b = (int)(it % kSlots);
+    const int64_t m = std::min<int64_t>(chunk, batch - off);
+    char* base = pool + slot * b;
+    float* dA = reinterpret_cast<float*>(base);
+    float* dL = reinterpret_cast<float*>(base + szA);
+    float* dV = vecs ? reinterpret_cast<float*>(base + szA + szL) : nullptr;
+    int32_t* dS = reinterpret_cast<int32_t*>(base + szA + szL + szV);
+    int32_t* dK = reinterpret_cast<int32_t*>(base + szA + szL + szV + szI);
+    // H2D: slot b's input is free once the solve of chunk it - kSlots is done
+    if (used[b] && (e = cudaStreamWaitEvent(st[H], ev[C][b], 0)) != cudaSuccess) { out = cuda_fail(e, "wait"); break; }
+    if ((e = cudaMemcpyAsync(dA, A + off * nn, sizeof(float) * m * nn, cudaMemcpyHostToDevice, st[H])) != cudaSuccess ||
+        (e = cudaEventRecord(ev[H][b], st[H])) != cudaSuccess) { out = cuda_fail(e, "H2D"); break; }
+    // solve: after this chunk's input arrived and slot b's outputs were read back
+    if ((e = cudaStreamWaitEvent(st[C], ev[H][b], 0)) != cudaSuccess ||
+        (used[b] && (e = cudaStreamWaitEvent(st[C], ev[D][b], 0)) != cudaSuccess)) { out = cuda_fail(e, "wait"); break; }
+    bed::FwdArgs a{dA, m, n, dL, dV, dS, dK, nullptr, kernel_cfg(cfg, n), st[C]};
+    if ((e = dispatch_forward(a)) != cudaSuccess) { out = cuda_fail(e, "bed_forward_host_f32 launch"); break; }
+    if ((e = cudaEventRecord(ev[C][b], st[C])) != cudaSuccess) { out = cuda_fail(e, "record"); break; }
+    // D2H
+    if ((e = cudaStreamWaitEvent(st[D], ev[C][b], 0)) != cudaSuccess ||
+        (vecs && (e = cudaMemcpyAsync(evecs + off * nn, dV, sizeof(float) * m * nn, cudaMemcpyDeviceToHost, st[D])) != cudaSuccess) ||
+        (e = cudaMemcpyAsync(evals + off * n, dL, sizeof(float) * m * n, cudaMemcpyDeviceToHost, st[D])) != cudaSuccess ||
+        (status && (e = cudaMemcpyAsync(status + off, dS, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st[D])) != cudaSuccess) ||
+        (steps && (e = cudaMemcpyAsync(steps + off, dK, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st[D])) != cudaSuccess) ||
+        (e = cudaEventRecord(ev[D][b], st[D])) != cudaSuccess) { out = cuda_fail(e, "D2H"); break; }
+    used[b] = true;
   }
-  for (int i = 0; i < kStreams; ++i) {
-    if (!streams[i]) continue;
-    if (dA[i]) cudaFreeAsync(dA[i], streams[i]);
-    if (dL[i]) cudaFreeAsync(dL[i], streams[i]);
-    if (dV[i]) cudaFreeAsync(dV[i], streams[i]);
-    if (dS[i]) cudaFreeAsync(dS[i], streams[i]);
-    if (dK[i]) cudaFreeAsync(dK[i], streams[i]);
-    e = cudaStreamSynchronize(streams[i]);
+  for (int r = 0; r < 3; ++r) {
+    if (!st[r]) continue;
+    e = cudaStreamSynchronize(st[r]);
     if (e != cudaSuccess && out == BED_SUCCESS) out = cuda_fail(e, "bed_forward_host_f32 sync");
-    cudaStreamDestroy(streams[i]);
+  }
+  if (pool) cudaFreeAsync(pool, st[C]);
+  if (st[C]) cudaStreamSynchronize(st[C]);
+  for (int r = 0; r < 3; ++r) {
+    for (int b = 0; b < kSlots; ++b)
+      if (ev[r][b]) cudaEventDestroy(ev[r][b]);
+    if (st[r]) cudaStreamDestroy(st[r]);
   }
   cudaSetDevice(prev);
   return out;
