@@ -237,15 +237,16 @@ __global__ void __launch_bounds__(kQThreads)
 template <int NMAX>
 struct FoldParams {
   static constexpr int L = GroupSize<NMAX>::L;
-  static constexpr int G = NMAX <= 32 ? 32 : 8;
+  static constexpr int G = NMAX <= 16 ? 32 : (NMAX <= 32 ? 16 : 8);
   static constexpr int THREADS = G * L;
   static constexpr int SROW = NMAX + 1;
   static constexpr int SMAT = NMAX * SROW;
   static constexpr int PADPOS = ((NMAX - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk;
+  static constexpr int K = 4;                                      // sweeps per phase
   static constexpr int RROW = PADPOS + 2;                          // float2 per matrix row
-  static constexpr int OFF_ROT = G * SMAT + (G * SMAT) % 4;        // float2 [2][G][RROW]
-  static constexpr int OFF_MM = OFF_ROT + 2 * 2 * G * RROW;       // int [2][G]
-  static constexpr int OFF_FLIP = OFF_MM + 2 * G;
+  static constexpr int OFF_ROT = G * SMAT + (G * SMAT) % 4;        // float2 [2][K][G][RROW]
+  static constexpr int OFF_MM = OFF_ROT + 2 * 2 * K * G * RROW;   // int [2][K][G]
+  static constexpr int OFF_FLIP = OFF_MM + 2 * K * G;
   static constexpr int OFF_EV = OFF_FLIP + G * NMAX;
   static constexpr int OFF_RANK = OFF_EV + G * NMAX;
   static constexpr int OFF_LAM = OFF_RANK + G * NMAX;
@@ -291,76 +292,88 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
   const int nrec = ws.nsw[w];
   const int* mws = ws.msw + (size_t)w * ws.Smax;
   const float2* recw = ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane0;
-  // thread t stages elements t, t + THREADS, ... of the sweep's [PADPOS][G]
-  // block (global order: position-major, lanes contiguous) into the
-  // matrix-major shared buffer [G][RROW], so a group reads two consecutive
-  // rotations with one 128-bit broadcast
+  // The stream is consumed in phases of K sweeps: one barrier per phase,
+  // and the next phase's records are loaded into registers while the
+  // current one is folded (a global load has a phase of work to land).
+  // Thread t stages elements t, t + THREADS, ... of each sweep's
+  // [PADPOS][G] block (global order: position-major, lanes contiguous) into
+  // the matrix-major shared buffer [G][RROW], so a group reads two
+  // consecutive rotations with one 128-bit broadcast.
+  constexpr int K = P::K;
   int* mbuf = reinterpret_cast<int*>(smem + P::OFF_MM);
   const uint8_t* mls = ws.mlane + (size_t)w * ws.Smax * 32 + lane0;
-  float2 pf[P::PER_THREAD];
-  int pm = 0;
-  auto fetch = [&](int s2, int npos) {
-    const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
+  float2 pf[K][P::PER_THREAD];
+  int pm[K];
+  auto npos_of = [&](int mw) { return min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk); };
+  auto fetch = [&](int ph) {
 #pragma unroll
-    for (int q = 0; q < P::PER_THREAD; ++q) {
-      const int e = tid + q * P::THREADS;
-      const int p = e / G, g = e - p * G;
-      pf[q] = (p < npos) ? __ldg(rs + p * 32 + g) : make_float2(1.0f, 0.0f);
+    for (int kk = 0; kk < K; ++kk) {
+      const int s2 = ph * K + kk;
+      const int npos = s2 < nrec ? npos_of(__ldg(mws + s2)) : 0;
+      const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
+#pragma unroll
+      for (int q = 0; q < P::PER_THREAD; ++q) {
+        const int e = tid + q * P::THREADS;
+        const int p = e / G, g = e - p * G;
+        pf[kk][q] = (p < npos) ? __ldg(rs + p * 32 + g) : make_float2(1.0f, 0.0f);
+      }
+      pm[kk] = (tid < G && s2 < nrec) ? __ldg(mls + (size_t)s2 * 32 + tid) : 0;
     }
-    if (tid < G) pm = __ldg(mls + (size_t)s2 * 32 + tid);
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < P::PER_THREAD; ++q) {
-      const int e = tid + q * P::THREADS;
-      const int p = e / G, g = e - p * G;
-      if (e < P::PADPOS * G) rbuf[(buf * G + g) * P::RROW + p] = pf[q];
+    for (int kk = 0; kk < K; ++kk) {
+#pragma unroll
+      for (int q = 0; q < P::PER_THREAD; ++q) {
+        const int e = tid + q * P::THREADS;
+        const int p = e / G, g = e - p * G;
+        if (e < P::PADPOS * G) rbuf[((buf * K + kk) * G + g) * P::RROW + p] = pf[kk][q];
+      }
+      if (tid < G) mbuf[(buf * K + kk) * G + tid] = pm[kk];
     }
-    if (tid < G) mbuf[buf * G + tid] = pm;
   };
-  auto npos_of = [&](int mw) { return min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk); };
-  int mw_next = nrec > 0 ? __ldg(mws) : 0;
-  if (nrec > 0) {
-    fetch(0, npos_of(mw_next));
+  const int nph = (nrec + K - 1) / K;
+  if (nph > 0) {
+    fetch(0);
     stash(0);
   }
   __syncthreads();
 #pragma unroll 1
-  for (int s2 = 0; s2 < nrec; ++s2) {
-    const int buf = s2 & 1;
-    if (s2 + 1 < nrec) {  // prefetch the next sweep while this one is folded
-      mw_next = __ldg(mws + s2 + 1);
-      fetch(s2 + 1, npos_of(mw_next));
-    }
-    const int mm = mbuf[buf * G + mi];  // this matrix's active size (0: no-op sweep)
-    if (mlive && mm > 1) {
-      const float2* rs = rbuf + (buf * G + mi) * P::RROW;
-      static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bcst) {
-        constexpr int b0 = decltype(bcst)::value * kFoldBlk;
-        constexpr int b1 = b0 + kFoldBlk < NMAX - 1 ? b0 + kFoldBlk : NMAX - 1;
-        if (b0 < mm - 1) {
+  for (int ph = 0; ph < nph; ++ph) {
+    const int buf = ph & 1;
+    if (ph + 1 < nph) fetch(ph + 1);  // lands while this phase is folded
+#pragma unroll 1
+    for (int kk = 0; kk < K; ++kk) {
+      const int mm = mbuf[(buf * K + kk) * G + mi];  // this matrix's active size (0: no-op)
+      if (mlive && mm > 1) {
+        const float2* rs = rbuf + ((buf * K + kk) * G + mi) * P::RROW;
+        static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bcst) {
+          constexpr int b0 = decltype(bcst)::value * kFoldBlk;
+          constexpr int b1 = b0 + kFoldBlk < NMAX - 1 ? b0 + kFoldBlk : NMAX - 1;
+          if (b0 < mm - 1) {
 #pragma unroll
-          for (int p = b0; p < b1; p += 2) {
-            // two rotations per 128-bit broadcast; scalar FMAs on purpose:
-            // the packed form (FMUL2 -> FFMA2) lengthens the position-to-
-            // position dependency chain and doubles the row's register
-            // footprint, which measured slower here
-            const float4 c2 = *reinterpret_cast<const float4*>(rs + p);
-            {
-              const float x = v[p], y = v[p + 1];
-              v[p] = c2.x * x - c2.y * y;
-              v[p + 1] = fmaf(c2.y, x, c2.x * y);
-            }
-            if (p + 1 < b1) {
-              const float x = v[p + 1], y = v[p + 2];
-              v[p + 1] = c2.z * x - c2.w * y;
-              v[p + 2] = fmaf(c2.w, x, c2.z * y);
+            for (int p = b0; p < b1; p += 2) {
+              // two rotations per 128-bit broadcast; scalar FMAs on purpose:
+              // the packed form (FMUL2 -> FFMA2) lengthens the position-to-
+              // position dependency chain and doubles the row's register
+              // footprint, which measured slower here
+              const float4 c2 = *reinterpret_cast<const float4*>(rs + p);
+              {
+                const float x = v[p], y = v[p + 1];
+                v[p] = c2.x * x - c2.y * y;
+                v[p + 1] = fmaf(c2.y, x, c2.x * y);
+              }
+              if (p + 1 < b1) {
+                const float x = v[p + 1], y = v[p + 2];
+                v[p + 1] = c2.z * x - c2.w * y;
+                v[p + 2] = fmaf(c2.w, x, c2.z * y);
+              }
             }
           }
-        }
-      });
+        });
+      }
     }
-    if (s2 + 1 < nrec) stash(buf ^ 1);
+    if (ph + 1 < nph) stash(buf ^ 1);
     __syncthreads();
   }
 
