@@ -10,26 +10,60 @@
 // (PAPER.md:668, :700).  The float64 restatement checked against this
 // kernel is oracle/oracle.py:taylor_backward.
 //
-// Layout: NMAX threads per matrix, thread i owns row i of every n x n
-// product; MB matrices per CTA.  Three n^3 FFMA products, all operands
-// staged in shared memory with 16-byte-aligned rows so the broadcast
-// operand reads are LDS.128; the final symmetrisation reads the transpose
-// through an odd stride (conflict free); loads and stores are coalesced.
+// Three n x n x n products per matrix, FP32 on the FMA pipe (no tensor
+// cores: the gradient gate is 1e-4 relative, beyond TF32):
+//   M = V^T gV      (then M' = F o M + diag(gL), F built in the epilogue)
+//   W = V M'
+//   G = W V^T       (gA = (G + G^T) / 2 through the shared stage)
+// Each thread owns a 4 x 4 output tile; per k it reads a 4-wide column slice
+// of A and a 4-wide row slice of B as two 128-bit shared loads and issues 8
+// FFMA2 (16 FMAs), so the products run at the FMA-pipe rate.  Every operand
+// is kept in the orientation its product reads: V, V^T, and the
+// intermediate results written transposed where the next product needs it.
 #pragma once
 
 #include "bed_common.cuh"
+#include "bed_f32x2.cuh"
+#include "bed_tile.cuh"
 
 namespace bed {
 
 template <int NMAX>
 struct BwdParams {
-  static constexpr int MB = NMAX >= 64 ? 2 : 256 / NMAX;
-  static constexpr int THREADS = MB * NMAX;
-  static constexpr int SA = NMAX + 4;  // aligned stride (broadcast / row reads)
-  static constexpr int SG = NMAX + 1;  // odd stride (transposed reads)
-  static constexpr int PER = 2 * NMAX * SA + 2 * NMAX;  // V, X stages + lam, inv
+  static constexpr int TQ = NMAX / 4;                 // tiles per row
+  static constexpr int TPM = TQ * TQ;                  // threads per matrix
+  static constexpr int MB = TPM >= 256 ? 1 : 256 / TPM;  // matrices per CTA
+  static constexpr int THREADS = MB * TPM;
+  static constexpr int SROW = NMAX + 4;                // 16-byte rows
+  static constexpr int SBUF = NMAX * SROW;
+  static constexpr int PER = 3 * SBUF + 2 * NMAX;      // V, V^T, X (gV -> M' -> G), lam, 1/lam
   static constexpr size_t BYTES = sizeof(float) * (size_t)MB * PER;
 };
+
+// acc (4 x 4 tile as [row][col pair]) += A(rows, k) B(k, cols) over k, with
+// At the k-major copy of A (At + k*SROW + r is A(r, k)) and B row-major.
+template <int NMAX, int SROW>
+__device__ __forceinline__ void tile_gemm(const float* At, const float* B, int ti, int tj,
+                                          f2 (&acc)[4][2]) {
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) {
+    const float4 a = *reinterpret_cast<const float4*>(At + k * SROW + 4 * ti);
+    const float4 b = *reinterpret_cast<const float4*>(B + k * SROW + 4 * tj);
+    const f2 b0 = f2_make(b.x, b.y), b1 = f2_make(b.z, b.w);
+    acc[0][0] = ffma2(f2_bc(a.x), b0, acc[0][0]);
+    acc[0][1] = ffma2(f2_bc(a.x), b1, acc[0][1]);
+    acc[1][0] = ffma2(f2_bc(a.y), b0, acc[1][0]);
+    acc[1][1] = ffma2(f2_bc(a.y), b1, acc[1][1]);
+    acc[2][0] = ffma2(f2_bc(a.z), b0, acc[2][0]);
+    acc[2][1] = ffma2(f2_bc(a.z), b1, acc[2][1]);
+    acc[3][0] = ffma2(f2_bc(a.w), b0, acc[3][0]);
+    acc[3][1] = ffma2(f2_bc(a.w), b1, acc[3][1]);
+  }
+}
+
+__device__ __forceinline__ float tile_at(const f2 (&acc)[4][2], int i, int j) {
+  return (j & 1) ? f2_hi(acc[i][j >> 1]) : f2_lo(acc[i][j >> 1]);
+}
 
 template <int NMAX, bool EXACT>
 __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
@@ -37,144 +71,123 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
                         const float* __restrict__ gV, const float* __restrict__ gL,
                         float* __restrict__ gA, int64_t batch, int n_rt, int degree) {
   using P = BwdParams<NMAX>;
-  constexpr int SA = P::SA, SG = P::SG;
+  constexpr int SROW = P::SROW, TQ = P::TQ;
   const int n = EXACT ? NMAX : n_rt;
   const int nn = n * n;
   extern __shared__ __align__(16) float smem[];
   const int tid = threadIdx.x;
-  const int mi = tid / NMAX;
-  const int row = tid % NMAX;
+  const int mi = tid / P::TPM;
+  const int t = tid % P::TPM;
+  const int ti = t / TQ, tj = t % TQ;
   const int64_t base = (int64_t)blockIdx.x * P::MB;
   const int count = (batch - base) < P::MB ? (int)(batch - base) : P::MB;
-  float* sV = smem + mi * P::PER;
-  float* sX = sV + NMAX * SA;
-  float* sL = sX + NMAX * SA;
+  float* sV = smem + mi * P::PER;  // V, row-major
+  float* sT = sV + P::SBUF;        // V^T, later read as the B of G = W V^T
+  float* sX = sT + P::SBUF;        // gV -> M' -> G
+  float* sL = sX + P::SBUF;
   float* sI = sL + NMAX;
 
   if (!EXACT) {  // padding rows/columns must read as zeros in the products
     for (int g = tid; g < P::MB * P::PER; g += P::THREADS) smem[g] = 0.0f;
     __syncthreads();
   }
-  // ---- coalesced loads of V and gV, plus the eigenvalues
-  for (int g = tid; g < count * nn; g += P::THREADS) {
-    int mat = g / nn, off = g - mat * nn;
-    int r = off / n, c = off - r * n;
-    float* dv = smem + mat * P::PER;
-    dv[r * SA + c] = __ldg(V + base * nn + g);
-    dv[NMAX * SA + r * SA + c] = gV ? __ldg(gV + base * nn + g) : 0.0f;
-  }
+  // ---- coalesced loads of V and gV into the stage, eigenvalues
+  // (the generic copy targets one buffer per matrix at stride PER)
+  tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
+  if (gV) tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(gV + base * nn, count, n, smem + 2 * P::SBUF);
   for (int g = tid; g < count * n; g += P::THREADS) {
-    int mat = g / n, c = g - mat * n;
-    float l = __ldg(lam + base * n + g);
-    float* dl = smem + mat * P::PER + 2 * NMAX * SA;
+    const int mat = g / n, c = g - mat * n;
+    const float l = __ldg(lam + base * n + g);
+    float* dl = smem + mat * P::PER + 3 * P::SBUF;
     dl[c] = l;
     dl[NMAX + c] = l != 0.0f ? 1.0f / l : 0.0f;
   }
   __syncthreads();
-
-  const bool live = mi < count && row < n;
-  // ---- M(row, :) = sum_r V(r, row) gV(r, :)
-  float acc[NMAX];
-#pragma unroll
-  for (int c = 0; c < NMAX; ++c) acc[c] = 0.0f;
-  if (gV && live) {
-    for (int r = 0; r < n; ++r) {
-      const float vr = sV[r * SA + row];
-      const float4* x4 = reinterpret_cast<const float4*>(sX + r * SA);
-#pragma unroll
-      for (int c4 = 0; c4 < NMAX / 4; ++c4) {
-        float4 x = x4[c4];
-        acc[4 * c4 + 0] = fmaf(vr, x.x, acc[4 * c4 + 0]);
-        acc[4 * c4 + 1] = fmaf(vr, x.y, acc[4 * c4 + 1]);
-        acc[4 * c4 + 2] = fmaf(vr, x.z, acc[4 * c4 + 2]);
-        acc[4 * c4 + 3] = fmaf(vr, x.w, acc[4 * c4 + 3]);
-      }
-    }
+  // V^T from V
+  for (int g = tid; g < P::MB * NMAX * NMAX; g += P::THREADS) {
+    const int mat = g / (NMAX * NMAX), off = g - mat * NMAX * NMAX;
+    const int r = off / NMAX, c = off - r * NMAX;
+    float* b = smem + mat * P::PER;
+    b[P::SBUF + c * SROW + r] = b[r * SROW + c];
   }
-  // ---- M' = F o M + diag(gL)
-  if (live) {
-    const float li = sL[row];
+  __syncthreads();
+
+  const bool live = mi < count;
+  f2 acc[4][2];
+  // ---- M = V^T gV, then M' = F o M + diag(gL) in the epilogue
 #pragma unroll
-    for (int c = 0; c < NMAX; ++c) {
-      if (c < n) {
-        float f = 0.0f;
-        if (c != row) {
-          const float lc = sL[c];
-          const bool hi_first = row < c ? (li >= lc) : (li > lc);
-          const float big_inv = hi_first ? sI[row] : sI[c];
-          const float small = hi_first ? lc : li;
-          const float ratio = small * big_inv;
-          float poly = 1.0f;
-          for (int k = 0; k < degree; ++k) poly = fmaf(poly, ratio, 1.0f);
-          const float t = big_inv * poly;
-          f = hi_first ? -t : t;
-        }
-        acc[c] *= f;
-      } else {
-        acc[c] = 0.0f;
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
+  if (gV) tile_gemm<NMAX, SROW>(sV, sX, ti, tj, acc);
+  // F by Horner in packed pairs (two tile columns per FFMA2)
+  float mp[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int i = 4 * ti + ii;
+    const float li = sL[i], ii_inv = sI[i];
+    const float gli = (gL && i < n && ti == tj && live) ? __ldg(gL + (base + mi) * n + i) : 0.0f;
+#pragma unroll
+    for (int jp = 0; jp < 2; ++jp) {
+      float ratio[2], binv[2];
+      bool hf[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 4 * tj + 2 * jp + h;
+        const float lj = sL[j];
+        hf[h] = i < j ? (li >= lj) : (li > lj);
+        binv[h] = hf[h] ? ii_inv : sI[j];
+        ratio[h] = (hf[h] ? lj : li) * binv[h];
+      }
+      const f2 rt = f2_make(ratio[0], ratio[1]);
+      f2 poly = f2_bc(1.0f);
+      for (int k = 0; k < degree; ++k) poly = ffma2(poly, rt, f2_bc(1.0f));
+      const f2 tt = fmul2(poly, f2_make(binv[0], binv[1]));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jj = 2 * jp + h, j = 4 * tj + jj;
+        const float tv = h ? f2_hi(tt) : f2_lo(tt);
+        const float f = i == j ? 0.0f : (hf[h] ? -tv : tv);
+        mp[ii][jj] = f * tile_at(acc, ii, jj) + (i == j ? gli : 0.0f);
       }
     }
   }
   __syncthreads();  // every thread is done reading gV
-  if (mi < count) {
-    float* xr = sX + row * SA;
+  if (live) {
 #pragma unroll
-    for (int c = 0; c < NMAX; ++c) xr[c] = live ? acc[c] : 0.0f;
-    if (live && gL) xr[row] += __ldg(gL + (base + mi) * n + row);
+    for (int ii = 0; ii < 4; ++ii)
+      *reinterpret_cast<float4*>(sX + (4 * ti + ii) * SROW + 4 * tj) =
+          make_float4(mp[ii][0], mp[ii][1], mp[ii][2], mp[ii][3]);
   }
   __syncthreads();
 
-  // ---- W(row, :) = V(row, :) M'
-  float vrow[NMAX];
+  // ---- W = V M' (A = V, read k-major from V^T); W^T goes to sV
 #pragma unroll
-  for (int c = 0; c < NMAX; ++c) {
-    vrow[c] = live ? sV[row * SA + c] : 0.0f;
-    acc[c] = 0.0f;
-  }
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
+  tile_gemm<NMAX, SROW>(sT, sX, ti, tj, acc);
+  if (live) {
 #pragma unroll
-  for (int i = 0; i < NMAX; ++i) {
-    if (!EXACT && i >= n) break;
-    const float vi = vrow[i];
-    const float4* x4 = reinterpret_cast<const float4*>(sX + i * SA);
-#pragma unroll
-    for (int c4 = 0; c4 < NMAX / 4; ++c4) {
-      float4 x = x4[c4];
-      acc[4 * c4 + 0] = fmaf(vi, x.x, acc[4 * c4 + 0]);
-      acc[4 * c4 + 1] = fmaf(vi, x.y, acc[4 * c4 + 1]);
-      acc[4 * c4 + 2] = fmaf(vi, x.z, acc[4 * c4 + 2]);
-      acc[4 * c4 + 3] = fmaf(vi, x.w, acc[4 * c4 + 3]);
-    }
-  }
-  // ---- G(row, c) = sum_i W(row, i) V(c, i)
-  float gr[NMAX];
-#pragma unroll
-  for (int c = 0; c < NMAX; ++c) {
-    float s = 0.0f;
-    if (EXACT || c < n) {
-      const float4* v4 = reinterpret_cast<const float4*>(sV + c * SA);
-#pragma unroll
-      for (int i4 = 0; i4 < NMAX / 4; ++i4) {
-        float4 x = v4[i4];
-        s = fmaf(acc[4 * i4 + 0], x.x, s);
-        s = fmaf(acc[4 * i4 + 1], x.y, s);
-        s = fmaf(acc[4 * i4 + 2], x.z, s);
-        s = fmaf(acc[4 * i4 + 3], x.w, s);
-      }
-    }
-    gr[c] = s;
-  }
-  __syncthreads();  // done reading M' from sX
-  if (mi < count) {
-    float* gout = sX + row * SG;
-#pragma unroll
-    for (int c = 0; c < NMAX; ++c) gout[c] = gr[c];
+    for (int jj = 0; jj < 4; ++jj)
+      *reinterpret_cast<float4*>(sV + (4 * tj + jj) * SROW + 4 * ti) =
+          make_float4(tile_at(acc, 0, jj), tile_at(acc, 1, jj), tile_at(acc, 2, jj), tile_at(acc, 3, jj));
   }
   __syncthreads();
+
+  // ---- G = W V^T (A = W, k-major from W^T; B(j, c) = V(c, j) = V^T row j)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
+  tile_gemm<NMAX, SROW>(sV, sT, ti, tj, acc);
+  if (live) {  // sX (M') was last read by the W product, before the barrier
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+      *reinterpret_cast<float4*>(sX + (4 * ti + ii) * SROW + 4 * tj) =
+          make_float4(tile_at(acc, ii, 0), tile_at(acc, ii, 1), tile_at(acc, ii, 2), tile_at(acc, ii, 3));
+  }
+  __syncthreads();
+  // ---- gA = (G + G^T) / 2, coalesced
   for (int g = tid; g < count * nn; g += P::THREADS) {
-    int mat = g / nn, off = g - mat * nn;
-    int r = off / n, c = off - r * n;
-    const float* gs = smem + mat * P::PER + NMAX * SA;
-    gA[base * nn + g] = 0.5f * (gs[r * SG + c] + gs[c * SG + r]);
+    const int mat = g / nn, off = g - mat * nn;
+    const int r = off / n, c = off - r * n;
+    const float* gs = smem + mat * P::PER + 2 * P::SBUF;
+    gA[base * nn + g] = 0.5f * (gs[r * SROW + c] + gs[c * SROW + r]);
   }
 }
 
