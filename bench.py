@@ -36,7 +36,9 @@ HEADLINE = dict(name="c2_fwd_n4", n=4, batch=4194304, mode="fwd")
 # limit 2^-22) and a 4n double-step budget -- the profile whose results pass
 # the parity gates (tests/parity.py).
 TOL = 3e-12
-FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9  # FFMA, nominal at max clock
+# FP32 FMA-pipe peak measured on B200 with tools/ubench/ffma_peak.cu (FFMA2,
+# profiles/r01_fp32_peak.md); nominal 148 SM x 128 x 2 x 1.965 GHz = 74.4 TFLOP/s
+FP32_PEAK = 73.7e12
 
 
 def peaks():
@@ -62,7 +64,7 @@ def work_per_matrix(n: int, mode: str):
 def roofline(n, mode, batch, seconds, hbm_peak):
     flops, nbytes = work_per_matrix(n, mode)
     t_hbm = batch * nbytes / hbm_peak
-    t_f32 = batch * flops / FP32_PEAK_NOMINAL
+    t_f32 = batch * flops / FP32_PEAK
     bound = "hbm" if t_hbm >= t_f32 else "fp32"
     return bound, max(t_hbm, t_f32) / seconds, flops * batch, nbytes * batch
 
@@ -283,7 +285,8 @@ def run_ours(args):
                      "traffic": load_traffic("bed_small_kernel<4,1>"),
                      "kernel": "bed_small_kernel<4, true>", "peak_source": peak_src,
                      "bytes_per_matrix": work_per_matrix(n, "fwd")[1],
-                     "fp32_frac_nominal": flops / per_step / FP32_PEAK_NOMINAL},
+                     "fp32_frac": flops / per_step / FP32_PEAK,
+                     "fp32_peak": "73.7 TFLOP/s measured (profiles/r01_fp32_peak.md)"},
         "clocks": clk.summary(),
     }
     mean_steps = float(step.steps.float().mean())
