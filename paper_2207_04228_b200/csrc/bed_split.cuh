@@ -244,9 +244,9 @@ struct FoldParams {
   static constexpr int PADPOS = ((NMAX - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk;
   static constexpr int K = 4;                                      // sweeps per phase
   static constexpr int RROW = PADPOS + 2;                          // float2 per matrix row
-  static constexpr int OFF_ROT = G * SMAT + (G * SMAT) % 4;        // float2 [2][K][G][RROW]
-  static constexpr int OFF_MM = OFF_ROT + 2 * 2 * K * G * RROW;   // int [2][K][G]
-  static constexpr int OFF_FLIP = OFF_MM + 2 * K * G;
+  static constexpr int OFF_ROT = (G * SMAT + 3) / 4 * 4;           // float2 [2][K][G][RROW], 16-byte aligned
+  static constexpr int OFF_MM = OFF_ROT + 2 * 2 * K * G * RROW;   // uint8 [2][K][G]
+  static constexpr int OFF_FLIP = OFF_MM + (2 * K * G + 3) / 4;
   static constexpr int OFF_EV = OFF_FLIP + G * NMAX;
   static constexpr int OFF_RANK = OFF_EV + G * NMAX;
   static constexpr int OFF_LAM = OFF_RANK + G * NMAX;
@@ -292,59 +292,55 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
   const int nrec = ws.nsw[w];
   const int* mws = ws.msw + (size_t)w * ws.Smax;
   const float2* recw = ws.rot + (size_t)w * ws.Smax * (NMAX - 1) * 32 + lane0;
-  // The stream is consumed in phases of K sweeps: one barrier per phase,
-  // and the next phase's records are loaded into registers while the
-  // current one is folded (a global load has a phase of work to land).
-  // Thread t stages elements t, t + THREADS, ... of each sweep's
-  // [PADPOS][G] block (global order: position-major, lanes contiguous) into
-  // the matrix-major shared buffer [G][RROW], so a group reads two
-  // consecutive rotations with one 128-bit broadcast.
+  // The stream is consumed in phases of K sweeps with one barrier per
+  // phase: while a phase is folded, the next phase's records travel
+  // global -> shared by cp.async (no register staging), each thread moving
+  // the (position, lane) rotations it covers into the matrix-major buffer
+  // [G][RROW], so a group reads two consecutive rotations with one 128-bit
+  // broadcast.  Positions past a sweep's padded warp extent are never read
+  // (every group's blocks end at or before it), so they are not copied.
   constexpr int K = P::K;
-  int* mbuf = reinterpret_cast<int*>(smem + P::OFF_MM);
+  uint8_t* mbuf = reinterpret_cast<uint8_t*>(smem + P::OFF_MM);  // [2][K][G] active sizes
   const uint8_t* mls = ws.mlane + (size_t)w * ws.Smax * 32 + lane0;
-  float2 pf[K][P::PER_THREAD];
-  int pm[K];
-  auto npos_of = [&](int mw) { return min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk); };
-  auto fetch = [&](int ph) {
+  constexpr int REC = (NMAX - 1) * 32;  // float2 per sweep record
+  int q_pos[P::PER_THREAD], q_goff[P::PER_THREAD], q_soff[P::PER_THREAD];
+#pragma unroll
+  for (int q = 0; q < P::PER_THREAD; ++q) {
+    const int e = tid + q * P::THREADS;
+    const int pp = e / G, g = e - pp * G;
+    q_pos[q] = e < P::PADPOS * G ? pp : NMAX;
+    q_goff[q] = pp * 32 + g;
+    q_soff[q] = g * P::RROW + pp;
+  }
+  auto fetch = [&](int ph, int buf) {
+    const float2* rs = recw + (size_t)ph * K * REC;
 #pragma unroll
     for (int kk = 0; kk < K; ++kk) {
       const int s2 = ph * K + kk;
-      const int npos = s2 < nrec ? npos_of(__ldg(mws + s2)) : 0;
-      const float2* rs = recw + (size_t)s2 * (NMAX - 1) * 32;
+      if (s2 < nrec) {
+        const int mw = __ldg(mws + s2);
+        const int npos = min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk);
+        float2* rb = rbuf + (buf * K + kk) * G * P::RROW;
 #pragma unroll
-      for (int q = 0; q < P::PER_THREAD; ++q) {
-        const int e = tid + q * P::THREADS;
-        const int p = e / G, g = e - p * G;
-        pf[kk][q] = (p < npos) ? __ldg(rs + p * 32 + g) : make_float2(1.0f, 0.0f);
+        for (int q = 0; q < P::PER_THREAD; ++q)
+          if (q_pos[q] < npos) cp_async8(rb + q_soff[q], rs + kk * REC + q_goff[q]);
+        if (tid == 0) cp_async_bytes<G>(mbuf + (buf * K + kk) * G, mls + (size_t)s2 * 32);
       }
-      pm[kk] = (tid < G && s2 < nrec) ? __ldg(mls + (size_t)s2 * 32 + tid) : 0;
     }
-  };
-  auto stash = [&](int buf) {
-#pragma unroll
-    for (int kk = 0; kk < K; ++kk) {
-#pragma unroll
-      for (int q = 0; q < P::PER_THREAD; ++q) {
-        const int e = tid + q * P::THREADS;
-        const int p = e / G, g = e - p * G;
-        if (e < P::PADPOS * G) rbuf[((buf * K + kk) * G + g) * P::RROW + p] = pf[kk][q];
-      }
-      if (tid < G) mbuf[(buf * K + kk) * G + tid] = pm[kk];
-    }
+    cp_async_commit();
   };
   const int nph = (nrec + K - 1) / K;
-  if (nph > 0) {
-    fetch(0);
-    stash(0);
-  }
+  if (nph > 0) fetch(0, 0);
+  cp_async_wait_all();
   __syncthreads();
 #pragma unroll 1
   for (int ph = 0; ph < nph; ++ph) {
     const int buf = ph & 1;
-    if (ph + 1 < nph) fetch(ph + 1);  // lands while this phase is folded
+    if (ph + 1 < nph) fetch(ph + 1, buf ^ 1);  // lands while this phase is folded
 #pragma unroll 1
     for (int kk = 0; kk < K; ++kk) {
-      const int mm = mbuf[(buf * K + kk) * G + mi];  // this matrix's active size (0: no-op)
+      // this matrix's active size in the sweep (0: no-op; past nrec: 0)
+      const int mm = ph * K + kk < nrec ? mbuf[(buf * K + kk) * G + mi] : 0;
       if (mlive && mm > 1) {
         const float2* rs = rbuf + ((buf * K + kk) * G + mi) * P::RROW;
         static_for<0, (NMAX - 1 + kFoldBlk - 1) / kFoldBlk>([&](auto bcst) {
@@ -373,7 +369,7 @@ __global__ void __launch_bounds__(FoldParams<NMAX>::THREADS)
         });
       }
     }
-    if (ph + 1 < nph) stash(buf ^ 1);
+    cp_async_wait_all();
     __syncthreads();
   }
 

@@ -13,6 +13,27 @@
 
 namespace bed {
 
+// cp.async (Ampere+ LDGSTS): global -> shared without register staging.
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+// B in {4, 8, 16} bytes (both addresses B-aligned); larger B in 16-byte pieces
+template <int B>
+__device__ __forceinline__ void cp_async_bytes(void* sdst, const void* gsrc) {
+  static_assert(B == 4 || B == 8 || B % 16 == 0, "cp.async moves 4, 8 or 16 bytes");
+  if constexpr (B <= 16) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gsrc), "n"(B) : "memory");
+  } else {
+#pragma unroll
+    for (int o = 0; o < B; o += 16)
+      cp_async_bytes<16>(static_cast<char*>(sdst) + o, static_cast<const char*>(gsrc) + o);
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int NMAX, int THREADS, int SROW, int SMAT>
 __device__ __forceinline__ void tile_to_stage(const float* __restrict__ src, int count, int n,
                                               float* stage) {
