@@ -162,6 +162,58 @@ __device__ __forceinline__ int small_deflate(const float (&e)[N], int m, float e
   return m;
 }
 
+// n <= 4: a sweep over all N positions with no per-position masks.  A
+// lane's deflated couplings are exact zeros (small_deflate_zero), so its
+// rotations there are exact identities and the reduced block is swept as in
+// the masked form (bitwise: the retire formula with an identity rotation
+// reduces to the tail formula); positions past the block only see the
+// shift added and removed again, a rounding-level change of an already
+// locked diagonal entry.  A lane that is off (finished, or budget spent)
+// sweeps with mu = 0 and its leading coupling masked, which is an exact
+// no-op, so results never depend on the warp's other lanes.
+template <int N, bool VECS>
+__device__ __forceinline__ void small_sweep_full(float (&d)[N], float (&e)[N],
+                                                 f2 (&v)[SmallLayout<N>::NP][N], bool on,
+                                                 float mu) {
+  float dw = d[0] - mu, g = on ? e[0] : 0.0f;
+  float c1 = 1.0f, s1 = 0.0f, ns1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float ei = i == 0 ? g : (i < N - 1 ? e[i] : 0.0f);
+    float c, s, ns, r;
+    small_givens<false>(dw, ei, c, s, ns, r);
+    const float dn = (i + 1 < N ? d[i + 1] : 0.0f) - mu;
+    // (u, dw') = (c g - s dn, s g + c dn)
+    const f2 ud = ffma2(f2_make(-s, c), f2_bc(dn), fmul2(f2_make(c, s), f2_bc(g)));
+    if (i > 0) {
+      d[i - 1] = (c1 * (c2 * r1) - s1 * u1) + mu;
+      e[i - 1] = (i == 1 && !on) ? e[0] : ns1 * r;
+      small_fold<N, VECS>(v, i - 1, c1, s1, ns1);
+    }
+    if (i == N - 1) d[i] = c1 * dw + mu;  // tail of the last position
+    c2 = c1;
+    c1 = c;
+    s1 = s;
+    ns1 = ns;
+    r1 = r;
+    u1 = f2_lo(ud);
+    dw = f2_hi(ud);
+    if (i + 1 < N - 1) g = c1 * e[i + 1];
+  }
+}
+
+// Deflation that also zeroes the couplings it locks (see small_sweep_full).
+template <int N>
+__device__ __forceinline__ int small_deflate_zero(float (&e)[N], int m, float eps) {
+#pragma unroll
+  for (int j = N - 2; j >= 1; --j) {
+    const bool dec = (m == j + 2) && (fabsf(e[j]) < eps);
+    m -= dec ? 1 : 0;
+    e[j] = dec ? 0.0f : e[j];
+  }
+  return m;
+}
+
 template <int N, bool VECS>
 __global__ void __launch_bounds__(kSmallThreads)
     bed_small_kernel(const float* __restrict__ A, int64_t batch, float* __restrict__ evals,
@@ -337,11 +389,43 @@ __global__ void __launch_bounds__(kSmallThreads)
   // ---- double-shift QR with per-matrix deflation, warp-synchronous
   int steps = 0;
   if constexpr (N >= 3) {
-    int m = small_deflate<N>(e, N, cfg.eps);
-    bool run = m > 2;
-    auto phase = [&](auto mac) {
-      constexpr int MA = decltype(mac)::value;
-      while (warp_any(run) && (MA == 3 || SweepSkip<N>::value || warp_any(m == MA))) {
+    if constexpr (N <= 4) {
+      int m = small_deflate_zero<N>(e, N, cfg.eps);
+      bool run = m > 2;
+      while (warp_any(run)) {
+        if (warp_any(run && steps >= cfg.max_steps)) {  // budget exhausted: qr.py:604-612
+          if (run && steps >= cfg.max_steps) {
+            float resid = 0.0f;
+#pragma unroll
+            for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
+            if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
+            run = false;  // lock the diagonal; the leading 2x2 still closes below
+#pragma unroll
+            for (int j = 1; j < N - 1; ++j) e[j] = 0.0f;  // off lanes sweep as exact no-ops
+          }
+        }
+        float ta = 0.0f, tb = 0.0f, td = 0.0f;
+#pragma unroll
+        for (int j = 1; j < N - 1; ++j) {
+          const float w = (j == m - 2) ? 1.0f : 0.0f;
+          ta = fmaf(w, d[j], ta);
+          tb = fmaf(w, e[j], tb);
+          td = fmaf(w, d[j + 1], td);
+        }
+        float lo, hi;
+        wilkinson_shifts(ta, tb, td, lo, hi);
+        small_sweep_full<N, VECS>(d, e, v, run, run ? hi : 0.0f);
+        m = small_deflate_zero<N>(e, m, cfg.eps);
+        const bool on2 = run && m > 2;
+        small_sweep_full<N, VECS>(d, e, v, on2, on2 ? lo : 0.0f);
+        m = small_deflate_zero<N>(e, m, cfg.eps);
+        steps += run ? 1 : 0;
+        run = run && m > 2;
+      }
+    } else {
+      int m = small_deflate<N>(e, N, cfg.eps);
+      bool run = m > 2;
+      while (warp_any(run)) {
         if (warp_any(run && steps >= cfg.max_steps)) {  // budget exhausted: qr.py:604-612
           if (run && steps >= cfg.max_steps) {
             float resid = 0.0f;
@@ -351,9 +435,12 @@ __global__ void __launch_bounds__(kSmallThreads)
             run = false;  // lock the diagonal; the leading 2x2 still closes below
           }
         }
+        // trailing 2x2 of the active block; an arithmetic blend, not a
+        // select chain, so the compiler cannot fold it into a dynamically
+        // indexed (local-memory) load of d[m-2]
         float ta = 0.0f, tb = 0.0f, td = 0.0f;
 #pragma unroll
-        for (int j = 1; j < MA - 1; ++j) {
+        for (int j = 1; j < N - 1; ++j) {
           const float w = (j == m - 2) ? 1.0f : 0.0f;
           ta = fmaf(w, d[j], ta);
           tb = fmaf(w, e[j], tb);
@@ -361,18 +448,15 @@ __global__ void __launch_bounds__(kSmallThreads)
         }
         float lo, hi;
         wilkinson_shifts(ta, tb, td, lo, hi);
-        small_sweep<N, VECS, MA>(d, e, v, run ? m : 0, hi);
+        // finished lanes sweep nothing (m = 0); their couplings do not
+        // move, so the unconditional deflations leave their m unchanged
+        small_sweep<N, VECS>(d, e, v, run ? m : 0, hi);
         m = small_deflate<N>(e, m, cfg.eps);
-        small_sweep<N, VECS, MA>(d, e, v, (run && m > 2) ? m : 0, lo);
+        small_sweep<N, VECS>(d, e, v, (run && m > 2) ? m : 0, lo);
         m = small_deflate<N>(e, m, cfg.eps);
         steps += run ? 1 : 0;
         run = run && m > 2;
       }
-    };
-    if constexpr (SweepSkip<N>::value) {
-      phase(std::integral_constant<int, N>{});
-    } else {
-      static_for<0, N - 2>([&](auto kc) { phase(std::integral_constant<int, N - decltype(kc)::value>{}); });
     }
   }
   if constexpr (N >= 2) {
