@@ -16,10 +16,12 @@
 // one FMUL2 + one FFMA2.
 //
 // The QR loop runs warp-synchronously: all 32 lanes stay in the loop until
-// every lane's matrix has deflated, finished lanes run masked (no-op) sweeps,
-// and sweep positions beyond every lane's active block are skipped by a warp
-// vote.  That keeps the code straight-line (no per-lane control flow the
-// compiler could fold into dynamically indexed, local-memory register arrays).
+// every lane's matrix has deflated; finished lanes run exact no-op sweeps.
+// n <= 4 sweeps all positions unmasked (locked couplings are exact zeros,
+// small_sweep_full); 5 <= n <= 8 masks positions past each lane's block and
+// skips positions no lane needs by a warp vote.  That keeps the code
+// straight-line (no per-lane control flow the compiler could fold into
+// dynamically indexed, local-memory register arrays).
 //
 // Per-matrix pipeline (reference /root/reference/pkg/src/batchedeig):
 //   validate + symmetrise        core.py:286-309
@@ -102,30 +104,22 @@ __device__ __forceinline__ void small_givens(float dw, float e, float& c, float&
   r = live ? rr : dw;
 }
 
-// How sweeps avoid positions no lane of the warp needs.  n > 4: a warp vote
-// per position.  n <= 4: that branch costs register moves at every join (the
-// packed V pairs change homes), so the QR loop is instead compiled once per
-// warp-maximum active size MA = n, n-1, ..., 3, each copy sweeping exactly
-// MA positions; a warp moves to the next copy when no lane has m == MA.
-template <int N>
-struct SweepSkip {
-  static constexpr bool value = N > 4;
-};
-
 // One explicit shifted QR sweep of the leading m-block, fused exactly like
 // _sweep_block (rotation i-1 retires once rotation i exists), written as
 // predicated straight-line code: rotations at positions >= m-1 degenerate to
 // the identity and writes past the active block are masked with selects.
 // m = 0 makes the whole sweep a no-op (used for lanes whose matrix has
-// finished).  Only positions below MA (>= every lane's m) are processed.
-template <int N, bool VECS, int MA = N>
+// finished).  Positions no lane of the warp needs are skipped by a vote
+// (n > 4; for n <= 4 the branch would cost register moves of the packed V
+// at every join, see small_sweep_full).
+template <int N, bool VECS>
 __device__ __forceinline__ void small_sweep(float (&d)[N], float (&e)[N],
                                             f2 (&v)[SmallLayout<N>::NP][N], int m, float mu) {
   float dw = d[0] - mu, g = e[0];
   float c1 = 1.0f, s1 = 0.0f, ns1 = 0.0f, c2 = 1.0f, r1 = 0.0f, u1 = 0.0f;
 #pragma unroll
-  for (int i = 0; i < MA; ++i) {
-    if (SweepSkip<N>::value && i >= 2 && !warp_any(i <= m - 1)) break;
+  for (int i = 0; i < N; ++i) {
+    if (i >= 2 && !warp_any(i <= m - 1)) break;
     const bool act = i < m - 1;
     const float ei = (i < N - 1 && act) ? e[i] : 0.0f;
     float c, s, ns, r;
