@@ -35,11 +35,13 @@ namespace bed {
 
 template <int NMAX>
 struct HHParams {
-  static constexpr int L = NMAX <= 16 ? 16 : 32;  // lanes per matrix
-  static constexpr int R = (NMAX + 31) / 32;       // rows per lane
-  static constexpr int MINB = NMAX == 64 ? 1 : (NMAX <= 16 ? 4 : 3);  // CTAs per SM the register cap must allow
+  // two rows per lane (l and l + L): every shuffle reduction serves 32 / L
+  // matrices at once and each lane carries twice the FMA work between them
+  static constexpr int L = NMAX <= 16 ? 8 : (NMAX <= 32 ? 16 : 32);  // lanes per matrix
+  static constexpr int R = (NMAX + L - 1) / L;                      // rows per lane
+  static constexpr int MINB = NMAX == 64 ? 1 : 2;  // CTAs per SM the register cap must allow
   static constexpr int NP = NMAX / 2;              // column pairs per row
-  static constexpr int G = NMAX == 64 ? 4 : 256 / L;  // matrices per CTA
+  static constexpr int G = NMAX == 64 ? 4 : 256 / L;  // matrices per CTA (shared stage per matrix)
   static constexpr int THREADS = G * L;
   static constexpr int SROW = NMAX + 4;            // 16-byte rows, conflict-free row reads
   static constexpr int SMAT = NMAX * SROW + NMAX;  // stage / reflectors + q
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     float amax = 0.0f, asym = 0.0f;
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const int row = l + 32 * rr;
+      const int row = l + L * rr;
       const bool ok = mlive && row < NMAX;  // NMAX = 24: lanes 24..31 hold no row
       const float4* r4 = reinterpret_cast<const float4*>(st + (ok ? row : 0) * SROW);
 #pragma unroll
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     float ss = 0.0f;
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      x[rr] = (l + 32 * rr > i) ? col_of<NP>(a[rr], i) : 0.0f;
+      x[rr] = (l + L * rr > i) ? col_of<NP>(a[rr], i) : 0.0f;
       ss = fmaf(x[rr], x[rr], ss);
     }
     ss = group_sum<L>(ss, mask);
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     if (ss > 0x1p-120f) {
       // sigma = sign(x_0) ||x||, u0 = x_0 + sigma, ||u||^2 = 2 sigma u0
       // (householder.py:97-118; the tail is already at unit scale)
-      constexpr int pr = (i + 1) / 32, pl = (i + 1) % 32;
+      constexpr int pr = (i + 1) / L, pl = (i + 1) % L;
       const float pivot = __shfl_sync(mask, x[pr], pl, L);
       const float nrm = ss * rsqrt_nr(ss);
       const float sigma = pivot >= 0.0f ? nrm : -nrm;
@@ -177,8 +179,8 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       const float iu = rsqrt_nr(2.0f * sigma * u0);  // sigma, u0 share a sign
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        u[rr] = (l + 32 * rr == i + 1 ? u0 : x[rr]) * iu;  // x = 0 for rows <= i
-        if (l + 32 * rr < NMAX) urow[l + 32 * rr] = u[rr];
+        u[rr] = (l + L * rr == i + 1 ? u0 : x[rr]) * iu;  // x = 0 for rows <= i
+        if (l + L * rr < NMAX) urow[l + L * rr] = u[rr];
       }
       __syncwarp(mask);
       // p = 2 A u (two accumulators per row for ILP), K = u^T p, q = p - K u
@@ -209,8 +211,8 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       float q[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        q[rr] = (l + 32 * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
-        if (l + 32 * rr < NMAX) qv[l + 32 * rr] = q[rr];
+        q[rr] = (l + L * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
+        if (l + L * rr < NMAX) qv[l + L * rr] = q[rr];
       }
       __syncwarp(mask);
       // A <- A - q u^T - u q^T on columns >= i (u, q vanish on the rest)
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     } else {
 #pragma unroll
       for (int rr = 0; rr < R; ++rr)
-        if (l + 32 * rr < NMAX) urow[l + 32 * rr] = 0.0f;
+        if (l + L * rr < NMAX) urow[l + L * rr] = 0.0f;
     }
     __syncwarp(mask);
   });
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
   if (mlive) {
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const int row = l + 32 * rr;
+      const int row = l + L * rr;
       float dv = 0.0f, ev = 0.0f;
 #pragma unroll
       for (int c = 0; c < NMAX; ++c) {
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     for (int rr = 0; rr < R; ++rr)
 #pragma unroll
       for (int k = 0; k < NP; ++k)
-        v[rr][k] = f2_make(l + 32 * rr == 2 * k ? 1.0f : 0.0f, l + 32 * rr == 2 * k + 1 ? 1.0f : 0.0f);
+        v[rr][k] = f2_make(l + L * rr == 2 * k ? 1.0f : 0.0f, l + L * rr == 2 * k + 1 ? 1.0f : 0.0f);
     static_for<0, NMAX - 2>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       if (!EXACT && i >= n - 2) return;
@@ -300,8 +302,8 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     __syncwarp(mask);  // every lane is done reading reflectors
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      if (l + 32 * rr >= NMAX) continue;
-      float4* r4 = reinterpret_cast<float4*>(st + (l + 32 * rr) * SROW);
+      if (l + L * rr >= NMAX) continue;
+      float4* r4 = reinterpret_cast<float4*>(st + (l + L * rr) * SROW);
 #pragma unroll
       for (int k4 = 0; k4 < NMAX / 4; ++k4)
         r4[k4] = make_float4(f2_lo(v[rr][2 * k4]), f2_hi(v[rr][2 * k4]), f2_lo(v[rr][2 * k4 + 1]),
