@@ -44,6 +44,8 @@
 namespace bed {
 
 constexpr int kSmallThreads = 128;
+// largest n whose QR loop sweeps every position unmasked (small_sweep_full)
+constexpr int kUnmaskedMaxN = 4;  // n = 8 measured equal either way
 
 template <int N>
 struct SmallLayout {
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(kSmallThreads)
   // ---- double-shift QR with per-matrix deflation, warp-synchronous
   int steps = 0;
   if constexpr (N >= 3) {
-    if constexpr (N <= 4) {
+    if constexpr (N <= kUnmaskedMaxN) {
       int m = small_deflate_zero<N>(e, N, cfg.eps);
       bool run = m > 2;
       while (warp_any(run)) {
