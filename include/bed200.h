@@ -29,6 +29,9 @@
  *                          way the reference API is called (solver.py:79)
  *   bed_backward_f32       (absent in the reference: pkg/README.md:116-117)
  *                          ED backward with Taylor-K
+ *   bed_matrix_power_f32   matrix_power()           solver.py:115-143
+ *                          (the ED's spectral-
+ *                          function consumer, V diag(f(lambda)) V^T)
  *   bed_error_string       error text for the integer return codes; the
  *                          reference maps kernel status ints to exceptions
  *                          in qr.py:604-609 / oracle.py:76-79
@@ -58,6 +61,8 @@ extern "C" {
 #define BED_STATUS_NO_CONVERGENCE 1 /* budget exhausted, a coupling >= deflation_tol remains */
 #define BED_STATUS_NON_FINITE 2     /* NaN/Inf in the input matrix */
 #define BED_STATUS_NON_SYMMETRIC 3  /* max|a_ij-a_ji| > symmetry_tol * max(1, ||A||_F) */
+#define BED_STATUS_NON_POSITIVE 4   /* bed_matrix_power_f32: non-positive clamped eigenvalue
+                                       with a negative or fractional power (NonPositiveSpectrum) */
 
 #define BED_SORT_NONE 0
 #define BED_SORT_DESCENDING 1
@@ -100,6 +105,17 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
  * are nullable (zero cotangent); gA (batch,n,n) is written. Device pointers. */
 int bed_backward_f32(const float* V, const float* evals, const float* gV, const float* gL,
                      float* gA, int64_t batch, int32_t n, int32_t taylor_degree, void* stream);
+
+/* Spectral power  out = sym( V diag(max(evals, floor)^p) V^T )  of a decomposed
+ * batch (reference matrix_power, solver.py:115-143).  floor < 0 selects the
+ * reference default 1e-12 * max(evals) per matrix.  With p negative or
+ * fractional, a matrix whose clamped spectrum is not positive gets status
+ * BED_STATUS_NON_POSITIVE (and bit 1 << 4 in flags) and a zero output.
+ * V (batch,n,n), evals (batch,n) as returned by bed_forward_f32; out (batch,n,n);
+ * status (batch) and flags (1) nullable.  Device pointers, stream-ordered. */
+int bed_matrix_power_f32(const float* V, const float* evals, float* out, int32_t* status,
+                         int32_t* flags, int64_t batch, int32_t n, float p, float floor,
+                         void* stream);
 
 const char* bed_error_string(int code);
 const char* bed_last_cuda_error(void); /* thread-local text of the last BED_ERR_CUDA */

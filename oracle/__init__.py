@@ -15,6 +15,9 @@ Contents
                        (``pkg/README.md:116-117``): **parity unpinned** against
                        the reference; pinned instead by the known-answer
                        properties in ``tests/test_oracle_backward.py``.
+``matrix_power``       float64 restatement of the reference spectral power
+                       (``solver.py:115-143``), the checker of
+                       ``bed_matrix_power_f32``.
 ``gen_spd``            restatement of the reference input generator
                        (``bench.py:112-134``), bit-identical to it.
 """
@@ -27,6 +30,7 @@ from .oracle import (  # noqa: F401
     forward,
     gen_spd,
     library_path,
+    matrix_power,
     taylor_backward,
     taylor_k,
     wilkinson,

@@ -195,6 +195,26 @@ def taylor_backward(v, evals, g_v=None, g_evals=None, degree: int = 9) -> np.nda
     return (g + g.transpose(0, 2, 1)) / 2.0
 
 
+def matrix_power(v, evals, p: float, floor: float | None = None) -> np.ndarray:
+    """V diag(max(w, floor)^p) V^T, symmetrised -- reference ``matrix_power``
+    (solver.py:115-143), float64.  Returns (out, bad) where ``bad`` marks the
+    matrices whose clamped spectrum is not positive for a negative or
+    fractional p (the reference raises NonPositiveSpectrum on the first)."""
+    v = np.asarray(v, np.float64)
+    w = np.asarray(evals, np.float64)
+    if floor is None:
+        clamped = np.maximum(w, 1e-12 * w.max(axis=1, keepdims=True))
+    else:
+        clamped = np.maximum(w, floor)
+    needs_positive = p < 0 or not float(p).is_integer()
+    bad = (clamped.min(axis=1) <= 0) if needs_positive else np.zeros(len(w), bool)
+    with np.errstate(all="ignore"):
+        powered = np.where(bad[:, None], 0.0, clamped) ** p
+    powered[bad] = 0.0
+    out = (v * powered[:, None, :]) @ v.transpose(0, 2, 1)
+    return (out + out.transpose(0, 2, 1)) / 2.0, bad
+
+
 # ---------------------------------------------------------------------------
 # input generator
 

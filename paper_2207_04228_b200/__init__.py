@@ -9,6 +9,7 @@ sm_100a kernels of ``_lib/libbed200.so`` (C ABI: ``include/bed200.h``).
 
 from .core import (  # noqa: F401
     BatchedEigError,
+    BatchedMatrix,
     BatchedSymmetric,
     EigenResult,
     NoConvergence,
@@ -25,7 +26,9 @@ from .solver import (  # noqa: F401
     batched_eig,
     eigh,
     forward_into,
+    matrix_power,
     taylor_backward,
+    zca_whiten,
 )
 from .sharding import gather_shards, shard_bounds, shard_sizes, solve_shard  # noqa: F401
 

@@ -18,12 +18,14 @@ STATUS_OK = 0
 STATUS_NO_CONVERGENCE = 1
 STATUS_NON_FINITE = 2
 STATUS_NON_SYMMETRIC = 3
+STATUS_NON_POSITIVE = 4
 
 # every symbol include/bed200.h declares
 EXPORTS = (
     "bed_forward_f32",
     "bed_forward_host_f32",
     "bed_backward_f32",
+    "bed_matrix_power_f32",
     "bed_error_string",
     "bed_last_cuda_error",
     "bed_abi_version",
@@ -69,6 +71,9 @@ def lib() -> ctypes.CDLL:
     L.bed_forward_host_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, ctypes.POINTER(BedConfig), i32]
     L.bed_backward_f32.restype = ctypes.c_int
     L.bed_backward_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, i32, vp]
+    L.bed_matrix_power_f32.restype = ctypes.c_int
+    L.bed_matrix_power_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, ctypes.c_float,
+                                       ctypes.c_float, vp]
     L.bed_error_string.restype = ctypes.c_char_p
     L.bed_error_string.argtypes = [ctypes.c_int]
     L.bed_last_cuda_error.restype = ctypes.c_char_p
@@ -116,3 +121,10 @@ def forward_host_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_pt
     rc = lib().bed_forward_host_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr,
                                     ctypes.byref(cfg), device)
     check(rc, "bed_forward_host_f32")
+
+
+def matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n, p, floor,
+                     stream) -> None:
+    rc = lib().bed_matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n,
+                                    p, floor, stream)
+    check(rc, "bed_matrix_power_f32")

@@ -27,6 +27,7 @@ __all__ = [
     "NoConvergence",
     "NonPositiveSpectrum",
     "ShapeMismatch",
+    "BatchedMatrix",
     "BatchedSymmetric",
     "SolverConfig",
     "SolveDiagnostics",
@@ -89,6 +90,36 @@ class NonPositiveSpectrum(BatchedEigError):
 
 class ShapeMismatch(BatchedEigError):
     """Two batched operands disagree in batch size or matrix dimension (core.py:108-109)."""
+
+
+@dataclass(frozen=True)
+class BatchedMatrix:
+    """A batch of dense rectangular matrices, shape (batch, rows, cols) (core.py:150-173).
+
+    Holds a numpy array or a torch tensor (the device path keeps tensors on
+    the GPU).
+    """
+
+    data: Any
+
+    def __post_init__(self):
+        shape = tuple(self.data.shape)
+        if len(shape) != 3:
+            raise ShapeMismatch(f"expected (batch, rows, cols) array, got {shape}")
+        if min(shape) < 1:
+            raise ShapeMismatch(f"all dimensions must be positive, got {shape}")
+
+    @property
+    def batch(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def dim_rows(self) -> int:
+        return self.data.shape[1]
+
+    @property
+    def dim_cols(self) -> int:
+        return self.data.shape[2]
 
 
 @dataclass(frozen=True)

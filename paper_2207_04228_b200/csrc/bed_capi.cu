@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -131,6 +132,26 @@ int bed_backward_f32(const float* V, const float* evals, const float* gV, const 
   bed::BwdArgs a{V, evals, gV, gL, gA, batch, n, taylor_degree, static_cast<cudaStream_t>(stream)};
   cudaError_t e = bed::launch_backward(a);
   if (e != cudaSuccess) return cuda_fail(e, "bed_backward_f32 launch");
+  return BED_SUCCESS;
+}
+
+int bed_matrix_power_f32(const float* V, const float* evals, float* out, int32_t* status,
+                         int32_t* flags, int64_t batch, int32_t n, float p, float floor,
+                         void* stream) {
+  if (batch < 0 || n < 1 || n > 64 || !(p == p)) return BED_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!V || !evals || !out)) return BED_ERR_INVALID_ARGUMENT;
+  if (!aligned4(V) || !aligned4(evals) || !aligned4(out) || !aligned4(status) || !aligned4(flags))
+    return BED_ERR_MISALIGNED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags) {
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "bed_matrix_power_f32 memset(flags)");
+  }
+  if (batch == 0) return BED_SUCCESS;
+  const int needs_positive = (p < 0.0f || p != floorf(p)) ? 1 : 0;  // solver.py:133
+  bed::PowArgs a{V, evals, out, status, flags, batch, n, p, floor, needs_positive, s};
+  cudaError_t e = bed::launch_power(a);
+  if (e != cudaSuccess) return cuda_fail(e, "bed_matrix_power_f32 launch");
   return BED_SUCCESS;
 }
 

@@ -17,10 +17,12 @@ import torch
 
 from . import _native
 from .core import (
+    BatchedMatrix,
     BatchedSymmetric,
     EigenResult,
     NoConvergence,
     NonFinite,
+    NonPositiveSpectrum,
     NonSymmetric,
     ShapeMismatch,
     SolveDiagnostics,
@@ -28,7 +30,7 @@ from .core import (
 )
 
 __all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into",
-           "TAYLOR_DEGREE"]
+           "matrix_power", "zca_whiten", "TAYLOR_DEGREE"]
 
 TAYLOR_DEGREE = 9
 
@@ -185,3 +187,74 @@ def eigh(A: torch.Tensor, cfg: SolverConfig | None = None, degree: int = TAYLOR_
          check: bool = True):
     """(eigenvalues, eigenvectors) of a CUDA float32 batch, differentiable."""
     return BatchedEigFn.apply(A, cfg, degree, check)
+
+
+def _power_device(V: torch.Tensor, lam: torch.Tensor, p: float, floor: float | None):
+    V = _check_cuda_f32(V, "eigenvectors")
+    lam = _check_cuda_f32(lam, "eigenvalues")
+    b, n, _ = V.shape
+    out = torch.empty_like(V)
+    status = torch.empty((b,), device=V.device, dtype=torch.int32)
+    flags = torch.empty((1,), device=V.device, dtype=torch.int32)
+    with torch.cuda.device(V.device):
+        _native.matrix_power_f32(V.data_ptr(), lam.data_ptr(), out.data_ptr(), status.data_ptr(),
+                                 flags.data_ptr(), b, n, float(p),
+                                 -1.0 if floor is None else float(floor),
+                                 _stream_handle(V.device))
+    if int(flags.item()) & (1 << _native.STATUS_NON_POSITIVE):
+        k = int(torch.nonzero(status == _native.STATUS_NON_POSITIVE)[0, 0])
+        raise NonPositiveSpectrum(k, float(lam[k].min()))
+    return out
+
+
+def matrix_power(e: EigenResult, p: float, floor: float | None = None) -> BatchedMatrix:
+    """Spectral power V diag(max(w, floor)^p) V^T of a decomposed batch
+    (reference ``matrix_power``, solver.py:115-143), on the GPU
+    (``bed_matrix_power_f32``: one tiled FFMA2 product per matrix).
+
+    ``floor=None`` applies the default guard 1e-12 * lambda_max per matrix;
+    ``floor=0.0`` disables it, and a non-positive eigenvalue then raises
+    NonPositiveSpectrum whenever p is negative or fractional.  Device
+    (tensor) results stay on the device; numpy results come back float64.
+    """
+    if e.eigenvectors is None:
+        raise ValueError("matrix_power needs an EigenResult with eigenvectors")
+    if floor is not None and floor < 0:
+        raise ValueError("floor must be nonnegative")
+    if isinstance(e.eigenvectors, torch.Tensor):
+        return BatchedMatrix(_power_device(e.eigenvectors, e.eigenvalues, p, floor))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    V = torch.from_numpy(np.ascontiguousarray(e.eigenvectors, dtype=np.float32)).to(dev)
+    lam = torch.from_numpy(np.ascontiguousarray(e.eigenvalues, dtype=np.float32)).to(dev)
+    out = _power_device(V, lam, p, floor)
+    return BatchedMatrix(out.cpu().numpy().astype(np.float64))
+
+
+def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None) -> BatchedMatrix:
+    """ZCA whitening of (batch, channels, samples) features (reference
+    ``zca_whiten``, solver.py:146-169): the unnormalised scatter
+    (X - mu)(X - mu)^T + eps_reg I is decomposed on the GPU and its inverse
+    square root (``matrix_power(-0.5, floor=0)``) applied to the centred
+    features.  The scatter and the final product are torch batched matmuls
+    (the covariance producer is SURVEY.md 8(f) row 3, not fused yet).
+    """
+    if eps_reg < 0:
+        raise ValueError("eps_reg must be nonnegative")
+    data = x.data if isinstance(x, BatchedMatrix) else x
+    host = not isinstance(data, torch.Tensor)
+    t = torch.from_numpy(np.asarray(data, dtype=np.float32)) if host else data
+    if host:
+        t = t.to(torch.device("cuda", torch.cuda.current_device()))
+    finite = torch.isfinite(t)
+    if not bool(finite.all()):
+        b, i, j = (int(v) for v in torch.nonzero(~finite)[0])
+        raise NonFinite(b, (i, j))
+    centered = t - t.mean(dim=2, keepdim=True)
+    scatter = centered @ centered.transpose(1, 2)
+    scatter = 0.5 * (scatter + scatter.transpose(1, 2))
+    if eps_reg:
+        scatter = scatter + eps_reg * torch.eye(t.shape[1], device=t.device, dtype=t.dtype)
+    dec = batched_eig(scatter.contiguous(), cfg)
+    inv_root = matrix_power(dec, -0.5, floor=0.0).data
+    out = inv_root @ centered
+    return BatchedMatrix(out.cpu().numpy().astype(np.float64) if host else out)

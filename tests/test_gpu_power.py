@@ -1,0 +1,135 @@
+"""GPU parity of the spectral power (bed_matrix_power_f32) and ZCA whitening
+ against the float64 restatement oracle.matrix_power
+of the reference matrix_power (solver.py:115-143), plus the reference's own
+known answers for matrix_power / zca_whiten (pkg/tests/test_solver.py:139-260)
+at FP32 tolerances."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+ROOT_HALF = np.sqrt(0.5)
+
+
+@pytest.fixture(scope="module")
+def bed():
+    import paper_2207_04228_b200 as bed
+
+    return bed
+
+
+def _cov(b, n, m, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((b, n, m))
+    x = x - x.mean(axis=2, keepdims=True)
+    c = x @ x.transpose(0, 2, 1) / m + 1e-3 * np.eye(n)
+    return ((c + c.transpose(0, 2, 1)) / 2).astype(np.float32)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8, 12, 16, 24, 32, 40, 64])
+@pytest.mark.parametrize("p", [-0.5, 0.5, 1.0, 2.0, -1.0, 0.3])
+def test_power_matches_oracle_on_same_decomposition(bed, n, p):
+    a = _cov(37, n, 4 * n, 100 + n)
+    e = bed.batched_eig(torch.from_numpy(a).cuda(), bed.SolverConfig(deflation_tol=3e-12))
+    out = bed.matrix_power(e, p).data.cpu().numpy().astype(np.float64)
+    ref, bad = oracle.matrix_power(e.eigenvectors.cpu().numpy(), e.eigenvalues.cpu().numpy(), p)
+    assert not bad.any()
+    err = np.linalg.norm(out - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
+    assert err.max() <= 1e-5, err.max()
+    np.testing.assert_array_equal(out, out.transpose(0, 2, 1))  # symmetrised (solver.py:141)
+
+
+def test_power_default_and_explicit_floor(bed):
+    lam = torch.tensor([[1.0, 1e-30], [4.0, -2.0]], device="cuda")
+    V = torch.eye(2, device="cuda").expand(2, 2, 2).contiguous()
+    e = bed.EigenResult(lam, V, bed.SolveDiagnostics(0, -1.0, -1, -1, None))
+    out = bed.matrix_power(e, -0.5).data.cpu().numpy()  # floor 1e-12 * lambda_max
+    assert np.isfinite(out).all()
+    assert out[0, 1, 1] == pytest.approx(1e6, rel=1e-6)
+    assert out[1, 1, 1] == pytest.approx((4e-12) ** -0.5, rel=1e-6)
+    with pytest.raises(bed.NonPositiveSpectrum) as err:
+        bed.matrix_power(e, -0.5, floor=0.0)
+    assert err.value.batch_index == 1
+    assert err.value.min_eigenvalue == pytest.approx(-2.0)
+    sq = bed.matrix_power(e, 2.0, floor=0.0).data.cpu().numpy()  # integer powers: no check
+    np.testing.assert_allclose(sq[1], np.diag([16.0, 0.0]), rtol=1e-6)  # max(-2, 0)^2
+
+
+# ---- the reference's known answers (pkg/tests/test_solver.py), FP32 tolerances
+
+
+def test_identity_inverse_root(bed):
+    e = bed.batched_eig(bed.BatchedSymmetric(np.eye(4)[None]))
+    np.testing.assert_allclose(bed.matrix_power(e, -0.5).data[0], np.eye(4), atol=1e-6)
+
+
+def test_square_root_of_diagonal(bed):
+    e = bed.batched_eig(bed.BatchedSymmetric(np.diag([4.0, 9.0])[None]))
+    np.testing.assert_allclose(bed.matrix_power(e, 0.5).data[0], np.diag([2.0, 3.0]), atol=1e-6)
+
+
+def test_inverse_root_identity_check(bed):
+    rng = np.random.default_rng(6)
+    raw = rng.standard_normal((16, 6, 6))
+    spd = raw @ raw.transpose(0, 2, 1) + 6 * np.eye(6)
+    e = bed.batched_eig(bed.BatchedSymmetric(spd), bed.SolverConfig(deflation_tol=3e-12))
+    r = bed.matrix_power(e, -0.5).data
+    resid = np.linalg.norm(r @ spd @ r - np.eye(6), axis=(1, 2))
+    assert resid.max() <= 1e-5
+
+
+def test_first_power_reproduces(bed):
+    rng = np.random.default_rng(7)
+    raw = rng.standard_normal((8, 5, 5))
+    spd = raw @ raw.transpose(0, 2, 1) + 5 * np.eye(5)
+    e = bed.batched_eig(bed.BatchedSymmetric(spd), bed.SolverConfig(deflation_tol=3e-12))
+    out = bed.matrix_power(e, 1.0).data
+    resid = np.linalg.norm(out - spd, axis=(1, 2)) / np.linalg.norm(spd, axis=(1, 2))
+    assert resid.max() <= 1e-5
+
+
+def test_square_root_consistency(bed):
+    rng = np.random.default_rng(8)
+    raw = rng.standard_normal((8, 7, 7))
+    spd = raw @ raw.transpose(0, 2, 1) + 7 * np.eye(7)
+    e = bed.batched_eig(bed.BatchedSymmetric(spd), bed.SolverConfig(deflation_tol=3e-12))
+    half = bed.matrix_power(e, 0.5).data
+    resid = np.linalg.norm(half @ half - spd, axis=(1, 2)) / np.linalg.norm(spd, axis=(1, 2))
+    assert resid.max() <= 1e-5
+
+
+def test_requires_vectors_and_valid_floor(bed):
+    e = bed.batched_eig(bed.BatchedSymmetric(np.eye(3)[None]), bed.SolverConfig(compute_vectors=False))
+    with pytest.raises(ValueError):
+        bed.matrix_power(e, 0.5)
+    e = bed.batched_eig(bed.BatchedSymmetric(np.eye(2)[None]))
+    with pytest.raises(ValueError):
+        bed.matrix_power(e, 0.5, floor=-1.0)
+
+
+def test_zca_single_channel_unit_variance(bed):
+    out = bed.zca_whiten(bed.BatchedMatrix(np.array([[[1.0, -1.0]]])), 0.0)
+    np.testing.assert_allclose(out.data[0, 0], [ROOT_HALF, -ROOT_HALF], rtol=1e-6)
+
+
+def test_zca_recomputed_covariance_is_identity(bed):
+    rng = np.random.default_rng(11)
+    x = bed.BatchedMatrix(rng.standard_normal((4, 8, 256)))
+    out = bed.zca_whiten(x, 1e-5)
+    centered = out.data - out.data.mean(axis=2, keepdims=True)
+    cov = centered @ centered.transpose(0, 2, 1)
+    assert np.abs(cov - np.eye(8)).max() <= 1e-4
+
+
+def test_zca_device_tensor_stays_on_device(bed):
+    x = torch.randn(16, 16, 64, device="cuda")
+    out = bed.zca_whiten(x, 1e-3).data
+    assert out.is_cuda and out.shape == x.shape
+    c = out - out.mean(dim=2, keepdim=True)
+    cov = (c @ c.transpose(1, 2)).cpu().numpy()
+    # eps_reg shrinks the whitened scatter slightly below I
+    assert np.abs(cov - np.eye(16)).max() <= 1e-2
