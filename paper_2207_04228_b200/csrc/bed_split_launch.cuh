@@ -31,32 +31,43 @@ cudaError_t run_split(const FwdArgs& a) {
   const size_t per_warp = vecs ? (size_t)smax * (4 + 32) + 4 : 0;
   const int64_t want = (a.batch + 31) / 32 * 32;
   const size_t need = (size_t)want * (per + per_warp / 32 + 1);
+  // No per-call cudaMemGetInfo (it can take milliseconds and stalls the
+  // stream's feed): try the full budget and shrink only if the pool refuses.
   size_t budget = kSplitWorkspaceBytes;
-  if (need > (size_t(256) << 20)) {  // only large solves pay for the free-memory query
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min(budget, free_b / 4);
-  }
-  int64_t cap = (int64_t)(budget / (per + per_warp / 32 + 1));
-  int64_t Bc = std::max<int64_t>(32, std::min<int64_t>(cap, want) / 32 * 32);
-  const int64_t W = Bc / 32;
-
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off += align256(bytes);
-    return o;
+  int64_t Bc = 0, W = 0;
+  size_t off = 0, oP = 0, oD = 0, oE = 0, oL = 0, oV = 0, oR = 0, oM = 0, oN = 0, oML = 0;
+  auto plan = [&] {
+    const int64_t cap = (int64_t)(budget / (per + per_warp / 32 + 1));
+    Bc = std::max<int64_t>(32, std::min<int64_t>(cap, want) / 32 * 32);
+    W = Bc / 32;
+    off = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = off;
+      off += align256(bytes);
+      return o;
+    };
+    oP = vecs ? take(4 * (size_t)Bc * nn) : 0;
+    oD = take(4 * (size_t)Bc * n);
+    oE = take(4 * (size_t)Bc * n);
+    oL = vecs ? take(4 * (size_t)Bc * n) : 0;
+    oV = take(4 * (size_t)Bc);
+    oR = vecs ? take((size_t)W * smax * (NMAX - 1) * 32 * 8) : 0;
+    oM = vecs ? take((size_t)W * smax * 4) : 0;
+    oN = vecs ? take((size_t)W * 4) : 0;
+    oML = vecs ? take((size_t)W * smax * 32) : 0;
   };
-  const size_t oP = vecs ? take(4 * (size_t)Bc * nn) : 0;
-  const size_t oD = take(4 * (size_t)Bc * n);
-  const size_t oE = take(4 * (size_t)Bc * n);
-  const size_t oL = vecs ? take(4 * (size_t)Bc * n) : 0;
-  const size_t oV = take(4 * (size_t)Bc);
-  const size_t oR = vecs ? take((size_t)W * smax * (NMAX - 1) * 32 * 8) : 0;
-  const size_t oM = vecs ? take((size_t)W * smax * 4) : 0;
-  const size_t oN = vecs ? take((size_t)W * 4) : 0;
-  const size_t oML = vecs ? take((size_t)W * smax * 32) : 0;
+  plan();
+  (void)need;
   char* base = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), off, a.stream);
+  while (e == cudaErrorMemoryAllocation && Bc > 32) {
+    cudaGetLastError();  // clear the allocation error
+    size_t free_b = 0, total_b = 0;
+    budget = (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) ? std::min(budget / 2, free_b / 2)
+                                                                 : budget / 2;
+    plan();
+    e = cudaMallocAsync(reinterpret_cast<void**>(&base), off, a.stream);
+  }
   if (e != cudaSuccess) return e;
   SplitWs ws;
   ws.P = vecs ? reinterpret_cast<float*>(base + oP) : nullptr;
