@@ -35,31 +35,76 @@ namespace bed {
 
 template <int NMAX>
 struct HHParams {
-  // two rows per lane (l and l + L): every shuffle reduction serves 32 / L
-  // matrices at once and each lane carries twice the FMA work between them
-  static constexpr int L = NMAX <= 16 ? 8 : (NMAX <= 32 ? 16 : 32);  // lanes per matrix
+  // n <= 32: two rows per lane (l and l + L): every shuffle reduction serves
+  // 32 / L matrices at once and each lane carries twice the FMA work.
+  // n = 64: one row per lane over two warps (64 lanes), so a matrix needs
+  // ~100 registers per thread instead of ~250 and twice the warps are in
+  // flight; the two warps meet through shared memory and a named barrier.
+  static constexpr int L = NMAX <= 16 ? 8 : (NMAX <= 32 ? 16 : 64);  // lanes per matrix
   static constexpr int R = (NMAX + L - 1) / L;                      // rows per lane
-  static constexpr int MINB = NMAX == 64 ? 1 : 2;  // CTAs per SM the register cap must allow
+  static constexpr int MINB = 2;  // CTAs per SM the register cap must allow
   static constexpr int NP = NMAX / 2;              // column pairs per row
   static constexpr int G = NMAX == 64 ? 4 : 256 / L;  // matrices per CTA (shared stage per matrix)
   static constexpr int THREADS = G * L;
   static constexpr int SROW = NMAX + 4;            // 16-byte rows, conflict-free row reads
-  static constexpr int SMAT = NMAX * SROW + NMAX;  // stage / reflectors + q
+  static constexpr int SMAT = NMAX * SROW + NMAX + 8;  // stage / reflectors + q + scratch
   static constexpr size_t BYTES = sizeof(float) * (size_t)G * SMAT;
 };
 
+// Communication inside a matrix's lane group.  L <= 32: warp shuffles.
+// L = 64 (two warps): a warp reduction, then the two partials through
+// shared memory behind a named barrier (id 1 + matrix); two scratch slots
+// alternate so one barrier per reduction suffices.
 template <int L>
-__device__ __forceinline__ float group_sum(float x, unsigned mask) {
+struct HHGroup {
+  unsigned mask;
+  int bar;
+  float* red;  // 8 floats: [2 slots][2 warps] partials, [2 slots] broadcast
+  int slot = 0;
+  int l;
+  __device__ __forceinline__ void init(int tid, int mi, float* scratch) {
+    l = tid % L;
+    mask = L >= 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
+    bar = 1 + mi;
+    red = scratch;
+  }
+  __device__ __forceinline__ void sync() const {
+    if constexpr (L <= 32) __syncwarp(mask);
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(64) : "memory");
+  }
+  template <bool IS_MAX>
+  __device__ __forceinline__ float reduce(float x) {
+    constexpr int W = L <= 32 ? L : 32;
 #pragma unroll
-  for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o, L);
-  return x;
-}
-template <int L>
-__device__ __forceinline__ float group_max(float x, unsigned mask) {
-#pragma unroll
-  for (int o = L / 2; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(mask, x, o, L));
-  return x;
-}
+    for (int o = W / 2; o > 0; o >>= 1) {
+      const float y = __shfl_xor_sync(mask, x, o, W);
+      x = IS_MAX ? fmaxf(x, y) : x + y;
+    }
+    if constexpr (L == 64) {
+      float* rs = red + 2 * slot;
+      if ((l & 31) == 0) rs[l >> 5] = x;
+      sync();
+      x = IS_MAX ? fmaxf(rs[0], rs[1]) : rs[0] + rs[1];
+      slot ^= 1;
+    }
+    return x;
+  }
+  __device__ __forceinline__ float sum(float x) { return reduce<false>(x); }
+  __device__ __forceinline__ float max(float x) { return reduce<true>(x); }
+  // value x held by group lane src (compile-time at every call)
+  __device__ __forceinline__ float bcast(float x, int src) {
+    if constexpr (L <= 32) {
+      return __shfl_sync(mask, x, src, L);
+    } else {
+      float* rb = red + 4 + slot;
+      if (l == src) *rb = x;
+      sync();
+      const float v = *rb;
+      slot ^= 1;
+      return v;
+    }
+  }
+};
 
 // component c of a packed row (c a compile-time constant at every call)
 template <int NP>
@@ -78,13 +123,14 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
   const int tid = threadIdx.x;
   const int mi = tid / L;
   const int l = tid % L;
-  const unsigned mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((tid & 31) & ~(L - 1)));
   const int64_t j0 = (int64_t)blockIdx.x * G;
   const int count = (bc - j0) < G ? (int)(bc - j0) : G;
   const bool mlive = mi < count;
   const int64_t j = j0 + mi;
   float* st = smem + mi * P::SMAT;  // rows of A, later reflector rows, later P rows
   float* qv = st + NMAX * SROW;     // q of the current step
+  HHGroup<L> grp;
+  grp.init(tid, mi, qv + NMAX);
 
   {  // coalesced tile load into the 16-byte-row stage (padding zero-filled)
     if (!EXACT) {
@@ -124,9 +170,9 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         a[rr][2 * k4 + 1] = f2_make(0.5f * (xs[2] + ys[2]), 0.5f * (xs[3] + ys[3]));
       }
     }
-    finite = group_max<L>(finite ? 0.0f : 1.0f, mask) == 0.0f;
-    amax = group_max<L>(amax, mask);
-    asym = group_max<L>(asym, mask);
+    finite = grp.max(finite ? 0.0f : 1.0f) == 0.0f;
+    amax = grp.max(amax);
+    asym = grp.max(asym);
     prescale = 1.0f;
     if (finite) unscale = pow2_ceil(amax, &prescale);
     // ||A||_F of the prescaled matrix (entries <= 1: no overflow)
@@ -138,7 +184,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         const f2 y = fmul2(a[rr][k], f2_bc(prescale));
         fro2 = fmaf(f2_lo(y), f2_lo(y), fmaf(f2_hi(y), f2_hi(y), fro2));
       }
-    fro2 = group_sum<L>(fro2, mask);
+    fro2 = grp.sum(fro2);
     if (!finite) {
       status = kStatusNonFinite;
     } else if (asym > cfg.sym_tol * fmaxf(1.0f, sqrtf(fro2) * unscale)) {
@@ -150,7 +196,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
 #pragma unroll
       for (int k = 0; k < NP; ++k) a[rr][k] = fmul2(a[rr][k], f2_bc(f));
   }
-  __syncwarp(mask);  // stage rows are about to be reused for reflectors
+  grp.sync();  // stage rows are about to be reused for reflectors
 
   // ---- Householder reduction; reflector i stored in st row i.  The step
   // loop is expanded by template recursion so every column index is a
@@ -165,14 +211,14 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       x[rr] = (l + L * rr > i) ? col_of<NP>(a[rr], i) : 0.0f;
       ss = fmaf(x[rr], x[rr], ss);
     }
-    ss = group_sum<L>(ss, mask);
+    ss = grp.sum(ss);
     float* urow = st + i * SROW;
     float u[R];
     if (ss > 0x1p-120f) {
       // sigma = sign(x_0) ||x||, u0 = x_0 + sigma, ||u||^2 = 2 sigma u0
       // (householder.py:97-118; the tail is already at unit scale)
       constexpr int pr = (i + 1) / L, pl = (i + 1) % L;
-      const float pivot = __shfl_sync(mask, x[pr], pl, L);
+      const float pivot = grp.bcast(x[pr], pl);
       const float nrm = ss * rsqrt_nr(ss);
       const float sigma = pivot >= 0.0f ? nrm : -nrm;
       const float u0 = pivot + sigma;
@@ -182,7 +228,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         u[rr] = (l + L * rr == i + 1 ? u0 : x[rr]) * iu;  // x = 0 for rows <= i
         if (l + L * rr < NMAX) urow[l + L * rr] = u[rr];
       }
-      __syncwarp(mask);
+      grp.sync();
       // p = 2 A u (two accumulators per row for ILP), K = u^T p, q = p - K u
       constexpr int k0 = ((i + 1) / 2) & ~1;  // 16-byte aligned start; u = 0 below i+1
       float p[R];
@@ -207,14 +253,14 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
           kk = fmaf(u[rr], p[rr], kk);
         }
       }
-      kk = group_sum<L>(kk, mask);
+      kk = grp.sum(kk);
       float q[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         q[rr] = (l + L * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
         if (l + L * rr < NMAX) qv[l + L * rr] = q[rr];
       }
-      __syncwarp(mask);
+      grp.sync();
       // A <- A - q u^T - u q^T on columns >= i (u, q vanish on the rest)
       constexpr int k1 = (i / 2) & ~1;
 #pragma unroll
@@ -235,7 +281,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       for (int rr = 0; rr < R; ++rr)
         if (l + L * rr < NMAX) urow[l + L * rr] = 0.0f;
     }
-    __syncwarp(mask);
+    grp.sync();
   });
 
   // ---- band: D[r] = a(r, r), E[r-1] = a(r, r-1), picked with compares on
@@ -299,7 +345,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         }
       }
     });
-    __syncwarp(mask);  // every lane is done reading reflectors
+    grp.sync();  // every lane is done reading reflectors
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (l + L * rr >= NMAX) continue;
