@@ -10,7 +10,8 @@ from paper_2207_04228_b200.datagen import covariance_device, gen_spd_device  # n
 torch.cuda.set_device(0)
 cases = [(4, 1 << 22, False), (8, 1 << 20, False), (16, 65536, True), (32, 65536, False),
          (64, 8192, True)]
-which = sys.argv[1:] or None
+which = [x for x in sys.argv[1:] if x.isdigit()] or None
+power = "pow" in sys.argv
 for n, b, bwd in cases:
     if which and str(n) not in which:
         continue
@@ -19,6 +20,8 @@ for n, b, bwd in cases:
     lam = torch.empty((b, n), device="cuda")
     vec = torch.empty((b, n, n), device="cuda")
     bed.forward_into(a, cfg, lam, vec)
+    if power:
+        bed.matrix_power(bed.EigenResult(lam, vec, None), -0.5)
     if bwd:
         gv = torch.randn_like(vec)
         gl = torch.randn_like(lam)
