@@ -15,5 +15,9 @@ for n, b in ((3, 130), (4, 131), (8, 129), (9, 37), (16, 161), (24, 70), (32, 33
     lam, v = bed.eigh(a, bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n))
     (v.sum() + lam.sum()).backward()
     bed.batched_eig(a.detach(), bed.SolverConfig(compute_vectors=False, max_double_steps=4 * n))
+    bed.matrix_power(bed.EigenResult(lam.detach(), v.detach(), None), -0.5)
+# chunked host path and a batch above the medium path's sub-warp tails
+x = oracle.gen_spd(3000, 4, 1).astype(np.float32)
+bed.batched_eig(x, bed.SolverConfig(deflation_tol=3e-12))
 torch.cuda.synchronize()
 print("sanitize cases done")
