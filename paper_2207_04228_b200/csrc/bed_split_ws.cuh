@@ -7,7 +7,7 @@
 namespace bed {
 
 constexpr int kFoldBlk = 8;    // positions per static fold block
-constexpr int kQThreads = 128;
+constexpr int kQThreads = 32;  // one warp per CTA: small batches (n = 64) still reach every SM
 
 struct SplitWs {
   float* P;         // [bc][n][n] initial V (VECS)
