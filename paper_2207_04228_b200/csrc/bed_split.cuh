@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kQThreads)
 template <int NMAX>
 struct FoldParams {
   static constexpr int L = GroupSize<NMAX>::L;
-  static constexpr int G = NMAX <= 16 ? 32 : (NMAX <= 32 ? 16 : 8);
+  static constexpr int G = NMAX <= 16 ? 8 : (NMAX <= 32 ? 4 : 8);
   static constexpr int THREADS = G * L;
   static constexpr int SROW = NMAX + 1;
   static constexpr int SMAT = NMAX * SROW;
