@@ -42,9 +42,9 @@ struct HHParams {
   // flight; the two warps meet through shared memory and a named barrier.
   static constexpr int L = NMAX <= 16 ? 8 : (NMAX <= 32 ? 16 : 64);  // lanes per matrix
   static constexpr int R = (NMAX + L - 1) / L;                      // rows per lane
-  static constexpr int MINB = 2;  // CTAs per SM the register cap must allow
+  static constexpr int MINB = 4;  // CTAs per SM the register cap must allow (128 registers)
   static constexpr int NP = NMAX / 2;              // column pairs per row
-  static constexpr int G = NMAX == 64 ? 4 : 256 / L;  // matrices per CTA (shared stage per matrix)
+  static constexpr int G = NMAX == 64 ? 2 : 128 / L;  // matrices per CTA (shared stage per matrix)
   static constexpr int THREADS = G * L;
   static constexpr int SROW = NMAX + 4;            // 16-byte rows, conflict-free row reads
   static constexpr int SMAT = NMAX * SROW + NMAX + 8;  // stage / reflectors + q + scratch
