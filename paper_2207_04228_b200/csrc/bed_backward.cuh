@@ -32,7 +32,7 @@ template <int NMAX>
 struct BwdParams {
   static constexpr int TQ = NMAX / 4;                 // tiles per row
   static constexpr int TPM = TQ * TQ;                  // threads per matrix
-  static constexpr int MB = TPM >= 256 ? 1 : 256 / TPM;  // matrices per CTA
+  static constexpr int MB = TPM >= 128 ? 1 : 128 / TPM;  // matrices per CTA
   static constexpr int THREADS = MB * TPM;
   static constexpr int SROW = NMAX + 4;                // 16-byte rows
   static constexpr int SBUF = NMAX * SROW;

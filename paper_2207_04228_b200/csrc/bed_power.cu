@@ -22,7 +22,7 @@ template <int NMAX>
 struct PowParams {
   static constexpr int TQ = NMAX / 4;
   static constexpr int TPM = TQ * TQ;
-  static constexpr int MB = TPM >= 256 ? 1 : 256 / TPM;
+  static constexpr int MB = TPM >= 128 ? 1 : 128 / TPM;
   static constexpr int THREADS = MB * TPM;
   static constexpr int SROW = NMAX + 4;
   static constexpr int SBUF = NMAX * SROW;
