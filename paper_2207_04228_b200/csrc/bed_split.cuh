@@ -65,8 +65,10 @@ __device__ __forceinline__ int qr_sweep(float (&d)[NMAX], float (&e)[NMAX], int 
     givens(dw, ei, c, s, r);
     if (VECS && i < NMAX - 1) rec[i * 32] = make_float2(c, s);
     const float dn = (i + 1 < NMAX ? d[i + 1] : 0.0f) - mu;
-    const float un = c * g - s * dn;
-    const float dwn = fmaf(s, g, c * dn);
+    // (u, dw') = (c g - s dn, s g + c dn): one FMUL2 + one FFMA2
+    const f2 ud = ffma2(f2_make(-s, c), f2_bc(dn), fmul2(f2_make(c, s), f2_bc(g)));
+    const float un = f2_lo(ud);
+    const float dwn = f2_hi(ud);
     if (i > 0) {
       const bool wr = i <= m - 1;  // rotation i-1 was a real one
       const float dret = (c1 * (c2 * r1) - s1 * u1) + mu;
