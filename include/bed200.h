@@ -32,6 +32,8 @@
  *   bed_matrix_power_f32   matrix_power()           solver.py:115-143
  *                          (the ED's spectral-
  *                          function consumer, V diag(f(lambda)) V^T)
+ *   bed_scatter_f32        the scatter inside zca_whiten()  solver.py:161-166
+ *                          (covariance producer)
  *   bed_error_string       error text for the integer return codes; the
  *                          reference maps kernel status ints to exceptions
  *                          in qr.py:604-609 / oracle.py:76-79
@@ -116,6 +118,13 @@ int bed_backward_f32(const float* V, const float* evals, const float* gV, const 
 int bed_matrix_power_f32(const float* V, const float* evals, float* out, int32_t* status,
                          int32_t* flags, int64_t batch, int32_t n, float p, float floor,
                          void* stream);
+
+/* Covariance producer: out = sym((X - mu)(X - mu)^T) + eps I
+ * per matrix, X (batch, n, m) row-major FP32 (n channels <= 64, m >= 1 samples), mu the
+ * per-channel sample mean -- the scatter of the reference zca_whiten (solver.py:161-166).
+ * out (batch, n, n).  Device pointers, stream-ordered. */
+int bed_scatter_f32(const float* X, int64_t batch, int32_t n, int32_t m, float eps, float* out,
+                    void* stream);
 
 const char* bed_error_string(int code);
 const char* bed_last_cuda_error(void); /* thread-local text of the last BED_ERR_CUDA */

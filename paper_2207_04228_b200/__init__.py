@@ -27,6 +27,7 @@ from .solver import (  # noqa: F401
     eigh,
     forward_into,
     matrix_power,
+    scatter_matrices,
     taylor_backward,
     zca_whiten,
 )

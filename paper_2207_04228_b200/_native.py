@@ -26,6 +26,7 @@ EXPORTS = (
     "bed_forward_host_f32",
     "bed_backward_f32",
     "bed_matrix_power_f32",
+    "bed_scatter_f32",
     "bed_error_string",
     "bed_last_cuda_error",
     "bed_abi_version",
@@ -74,6 +75,8 @@ def lib() -> ctypes.CDLL:
     L.bed_matrix_power_f32.restype = ctypes.c_int
     L.bed_matrix_power_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, ctypes.c_float,
                                        ctypes.c_float, vp]
+    L.bed_scatter_f32.restype = ctypes.c_int
+    L.bed_scatter_f32.argtypes = [vp, i64, i32, i32, ctypes.c_float, vp, vp]
     L.bed_error_string.restype = ctypes.c_char_p
     L.bed_error_string.argtypes = [ctypes.c_int]
     L.bed_last_cuda_error.restype = ctypes.c_char_p
@@ -128,3 +131,8 @@ def matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n,
     rc = lib().bed_matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n,
                                     p, floor, stream)
     check(rc, "bed_matrix_power_f32")
+
+
+def scatter_f32(X_ptr, batch, n, m, eps, out_ptr, stream) -> None:
+    rc = lib().bed_scatter_f32(X_ptr, batch, n, m, eps, out_ptr, stream)
+    check(rc, "bed_scatter_f32")

@@ -155,6 +155,18 @@ int bed_matrix_power_f32(const float* V, const float* evals, float* out, int32_t
   return BED_SUCCESS;
 }
 
+int bed_scatter_f32(const float* X, int64_t batch, int32_t n, int32_t m, float eps, float* out,
+                    void* stream) {
+  if (batch < 0 || n < 1 || n > 64 || m < 1 || !(eps >= 0.0f)) return BED_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!X || !out)) return BED_ERR_INVALID_ARGUMENT;
+  if (!aligned4(X) || !aligned4(out)) return BED_ERR_MISALIGNED;
+  if (batch == 0) return BED_SUCCESS;
+  bed::ScatArgs a{X, out, batch, n, m, eps, static_cast<cudaStream_t>(stream)};
+  cudaError_t e = bed::launch_scatter(a);
+  if (e != cudaSuccess) return cuda_fail(e, "bed_scatter_f32 launch");
+  return BED_SUCCESS;
+}
+
 // Host-buffer entry: the batch streams through the device in chunks.  Three
 // role streams -- host-to-device copies, solves, device-to-host copies --
 // and a ring of kSlots device buffer sets ordered by events, so the copy

@@ -48,11 +48,22 @@ struct PowArgs {
   cudaStream_t stream;
 };
 
+struct ScatArgs {
+  const float* X;  // (batch, n, m)
+  float* out;      // (batch, n, n)
+  int64_t batch;
+  int n;
+  int m;
+  float eps;
+  cudaStream_t stream;
+};
+
 cudaError_t launch_small(const FwdArgs& a);      // 1 <= n <= 8   (bed_small.cu)
 cudaError_t launch_split16(const FwdArgs& a);    // 9 <= n <= 16  (bed_split16.cu)
 cudaError_t launch_split32(const FwdArgs& a);    // 17 <= n <= 32 (bed_split32.cu)
 cudaError_t launch_split64(const FwdArgs& a);    // 33 <= n <= 64 (bed_split64.cu)
 cudaError_t launch_backward(const BwdArgs& a);   // 1 <= n <= 64  (bed_backward.cu)
 cudaError_t launch_power(const PowArgs& a);      // 1 <= n <= 64  (bed_power.cu)
+cudaError_t launch_scatter(const ScatArgs& a);   // 1 <= n <= 64  (bed_scatter.cu)
 
 }  // namespace bed

@@ -1,0 +1,149 @@
+// bed_scatter.cu -- the covariance producer in front of the ED (SURVEY.md
+// 8(f) row 3): out = (X - mu)(X - mu)^T + eps I per matrix, X (batch, n, m)
+// row-major (n channels, m samples), mu the per-channel sample mean -- the
+// scatter of the reference zca_whiten (solver.py:161-166) and of
+// decorrelated BN / global covariance pooling.
+//
+// A CTA owns 128 / (NMAX/4)^2 matrices (one for n > 32): pass 1 reduces the channel means
+// (one warp per channel row, coalesced), pass 2 streams the centred
+// samples in chunks of KC through shared memory k-major (X_c^T) and
+// accumulates X_c X_c^T on the 4 x 4 FFMA2 register tiles of the backward
+// (both operands are the same k-major chunk).  The result is symmetrised
+// through the stage like the reference ((S + S^T) / 2, solver.py:164).
+#include "bed_backward.cuh"
+#include "bed_launch.h"
+
+namespace bed {
+
+template <int NMAX>
+struct ScatParams {
+  static constexpr int TQ = NMAX / 4;
+  static constexpr int TPM = TQ * TQ;                   // tile owners per matrix
+  static constexpr int MB = TPM >= 128 ? 1 : 128 / TPM;  // matrices per CTA
+  static constexpr int THREADS = MB * TPM;
+  static constexpr int KC = 32;                         // samples per staged chunk
+  static constexpr int SROW = NMAX + 4;
+  static constexpr int PER = KC * SROW + NMAX + NMAX * (NMAX + 1);  // X_c^T chunk, mu, result
+  static constexpr size_t BYTES = sizeof(float) * (size_t)MB * PER;
+};
+
+template <int NMAX>
+__device__ __forceinline__ void tile_gemm_chunk(const float* XT, int ti, int tj, int kc, f2 (&acc)[4][2]) {
+  constexpr int SROW = ScatParams<NMAX>::SROW;
+#pragma unroll 8
+  for (int k = 0; k < kc; ++k) {
+    const float4 a = *reinterpret_cast<const float4*>(XT + k * SROW + 4 * ti);
+    const float4 b = *reinterpret_cast<const float4*>(XT + k * SROW + 4 * tj);
+    const f2 b0 = f2_make(b.x, b.y), b1 = f2_make(b.z, b.w);
+    acc[0][0] = ffma2(f2_bc(a.x), b0, acc[0][0]);
+    acc[0][1] = ffma2(f2_bc(a.x), b1, acc[0][1]);
+    acc[1][0] = ffma2(f2_bc(a.y), b0, acc[1][0]);
+    acc[1][1] = ffma2(f2_bc(a.y), b1, acc[1][1]);
+    acc[2][0] = ffma2(f2_bc(a.z), b0, acc[2][0]);
+    acc[2][1] = ffma2(f2_bc(a.z), b1, acc[2][1]);
+    acc[3][0] = ffma2(f2_bc(a.w), b0, acc[3][0]);
+    acc[3][1] = ffma2(f2_bc(a.w), b1, acc[3][1]);
+  }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(ScatParams<NMAX>::THREADS)
+    bed_scatter_kernel(const float* __restrict__ X, float* __restrict__ out, int64_t batch, int n,
+                       int m, float eps) {
+  using P = ScatParams<NMAX>;
+  constexpr int SROW = P::SROW, TQ = P::TQ, KC = P::KC;
+  extern __shared__ __align__(16) float smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = P::THREADS / 32;
+  const int64_t base = (int64_t)blockIdx.x * P::MB;
+  const int count = (batch - base) < P::MB ? (int)(batch - base) : P::MB;
+  const float* x = X + base * n * m;
+  auto buf = [&](int mat) { return smem + mat * P::PER; };
+
+  // pass 1: channel means (warp per row, coalesced along samples)
+  for (int rr = warp; rr < P::MB * NMAX; rr += NWARP) {
+    const int mat = rr / NMAX, r = rr - mat * NMAX;
+    float s = 0.0f;
+    if (mat < count && r < n) {
+      const float* row = x + ((int64_t)mat * n + r) * m;
+      float s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+      int k = lane;
+      for (; k + 96 < m; k += 128) {
+        s += __ldg(row + k);
+        s1 += __ldg(row + k + 32);
+        s2 += __ldg(row + k + 64);
+        s3 += __ldg(row + k + 96);
+      }
+      for (; k < m; k += 32) s += __ldg(row + k);
+      s += (s1 + s2) + s3;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) buf(mat)[KC * SROW + r] = (mat < count && r < n) ? s / (float)m : 0.0f;
+  }
+  __syncthreads();
+
+  // pass 2: S = X_c X_c^T over chunks of KC samples staged k-major
+  const int mi = tid / P::TPM, t = tid % P::TPM;
+  const int ti = t / TQ, tj = t % TQ;
+  f2 acc[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
+  for (int k0 = 0; k0 < m; k0 += KC) {
+    const int kc = min(KC, m - k0);
+#pragma unroll 4
+    for (int g = tid; g < P::MB * NMAX * KC; g += P::THREADS) {  // coalesced along samples
+      const int rr = g / KC, k = g - rr * KC;
+      const int mat = rr / NMAX, r = rr - mat * NMAX;
+      float v = 0.0f;
+      if (mat < count && r < n && k < kc)
+        v = __ldg(x + ((int64_t)mat * n + r) * m + k0 + k) - buf(mat)[KC * SROW + r];
+      buf(mat)[k * SROW + r] = v;
+    }
+    __syncthreads();
+    tile_gemm_chunk<NMAX>(buf(mi), ti, tj, kc, acc);
+    __syncthreads();
+  }
+  float* cs = buf(mi) + KC * SROW + NMAX;
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) cs[(4 * ti + ii) * (NMAX + 1) + 4 * tj + jj] = tile_at(acc, ii, jj);
+  __syncthreads();
+  const int nn = n * n;
+  for (int g = tid; g < count * nn; g += P::THREADS) {
+    const int mat = g / nn, off = g - mat * nn;
+    const int r = off / n, c = off - r * n;
+    const float* c2 = buf(mat) + KC * SROW + NMAX;
+    float v = 0.5f * (c2[r * (NMAX + 1) + c] + c2[c * (NMAX + 1) + r]);
+    if (r == c) v += eps;
+    out[base * nn + g] = v;
+  }
+}
+
+template <int NMAX>
+static cudaError_t go_scatter(const ScatArgs& a) {
+  using P = ScatParams<NMAX>;
+  auto kern = bed_scatter_kernel<NMAX>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const unsigned grid = (unsigned)((a.batch + P::MB - 1) / P::MB);
+  kern<<<grid, P::THREADS, P::BYTES, a.stream>>>(a.X, a.out, a.batch, a.n, a.m, a.eps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const ScatArgs& a) {
+  if (a.n <= 4) return go_scatter<4>(a);
+  if (a.n <= 8) return go_scatter<8>(a);
+  if (a.n <= 16) return go_scatter<16>(a);
+  if (a.n <= 32) return go_scatter<32>(a);
+  return go_scatter<64>(a);
+}
+
+}  // namespace bed

@@ -30,7 +30,7 @@ from .core import (
 )
 
 __all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into",
-           "matrix_power", "zca_whiten", "TAYLOR_DEGREE"]
+           "matrix_power", "zca_whiten", "scatter_matrices", "TAYLOR_DEGREE"]
 
 TAYLOR_DEGREE = 9
 
@@ -230,6 +230,19 @@ def matrix_power(e: EigenResult, p: float, floor: float | None = None) -> Batche
     return BatchedMatrix(out.cpu().numpy().astype(np.float64))
 
 
+def scatter_matrices(x: torch.Tensor, eps: float = 0.0) -> torch.Tensor:
+    """sym((X - mu)(X - mu)^T) + eps I per matrix of a (batch, n, m) CUDA float32
+    batch (the scatter of the reference zca_whiten, solver.py:161-166), on the
+    native covariance producer ``bed_scatter_f32``."""
+    x = _check_cuda_f32(x, "X")
+    b, n, m = x.shape
+    out = torch.empty((b, n, n), device=x.device, dtype=torch.float32)
+    with torch.cuda.device(x.device):
+        _native.scatter_f32(x.data_ptr(), b, n, m, float(eps), out.data_ptr(),
+                            _stream_handle(x.device))
+    return out
+
+
 def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None) -> BatchedMatrix:
     """ZCA whitening of (batch, channels, samples) features (reference
     ``zca_whiten``, solver.py:146-169): the unnormalised scatter
@@ -249,12 +262,10 @@ def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None
     if not bool(finite.all()):
         b, i, j = (int(v) for v in torch.nonzero(~finite)[0])
         raise NonFinite(b, (i, j))
+    t = t.contiguous()
+    scatter = scatter_matrices(t, eps_reg)
     centered = t - t.mean(dim=2, keepdim=True)
-    scatter = centered @ centered.transpose(1, 2)
-    scatter = 0.5 * (scatter + scatter.transpose(1, 2))
-    if eps_reg:
-        scatter = scatter + eps_reg * torch.eye(t.shape[1], device=t.device, dtype=t.dtype)
-    dec = batched_eig(scatter.contiguous(), cfg)
+    dec = batched_eig(scatter, cfg)
     inv_root = matrix_power(dec, -0.5, floor=0.0).data
     out = inv_root @ centered
     return BatchedMatrix(out.cpu().numpy().astype(np.float64) if host else out)

@@ -133,3 +133,21 @@ def test_zca_device_tensor_stays_on_device(bed):
     cov = (c @ c.transpose(1, 2)).cpu().numpy()
     # eps_reg shrinks the whitened scatter slightly below I
     assert np.abs(cov - np.eye(16)).max() <= 1e-2
+
+
+# ---- covariance producer (bed_scatter_f32)
+
+
+@pytest.mark.parametrize("n,m", [(1, 5), (3, 7), (4, 64), (7, 33), (16, 64), (24, 100), (32, 31),
+                                 (40, 256), (64, 256), (64, 70)])
+@pytest.mark.parametrize("eps", [0.0, 1e-3])
+def test_scatter_matches_float64(bed, n, m, eps):
+    rng = np.random.default_rng(n * 1000 + m)
+    x = (rng.standard_normal((9, n, m)) * 3.0 + rng.standard_normal((9, n, 1)) * 10.0).astype(np.float32)
+    out = bed.scatter_matrices(torch.from_numpy(x).cuda(), eps).cpu().numpy().astype(np.float64)
+    xc = x.astype(np.float64) - x.astype(np.float64).mean(axis=2, keepdims=True)
+    ref = xc @ xc.transpose(0, 2, 1)
+    ref = (ref + ref.transpose(0, 2, 1)) / 2 + eps * np.eye(n)
+    err = np.linalg.norm(out - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
+    assert err.max() <= 1e-5, err.max()
+    np.testing.assert_array_equal(out, out.transpose(0, 2, 1))

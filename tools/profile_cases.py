@@ -12,6 +12,13 @@ cases = [(4, 1 << 22, False), (8, 1 << 20, False), (16, 65536, True), (32, 65536
          (64, 8192, True)]
 which = [x for x in sys.argv[1:] if x.isdigit()] or None
 power = "pow" in sys.argv
+if "scat" in sys.argv:  # covariance producer only
+    for n, m, b in ((16, 64, 65536), (64, 256, 8192)):
+        x = torch.randn((b, n, m), device="cuda")
+        bed.scatter_matrices(x, 1e-5)
+    torch.cuda.synchronize()
+    print("done")
+    sys.exit(0)
 for n, b, bwd in cases:
     if which and str(n) not in which:
         continue
