@@ -8,7 +8,10 @@ sm_100a kernels of ``_lib/libbed200.so`` (C ABI: ``include/bed200.h``).
 """
 
 from .core import (  # noqa: F401
+    BadMagic,
     BatchedEigError,
+    DimMismatch,
+    TruncatedPayload,
     BatchedMatrix,
     BatchedSymmetric,
     EigenResult,
@@ -31,6 +34,7 @@ from .solver import (  # noqa: F401
     taylor_backward,
     zca_whiten,
 )
+from .bed_io import read_batch, read_matrix, write_batch  # noqa: F401
 from .sharding import gather_shards, shard_bounds, shard_sizes, solve_shard  # noqa: F401
 
 __version__ = "0.1.0"

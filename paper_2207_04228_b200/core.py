@@ -26,6 +26,9 @@ __all__ = [
     "NonFinite",
     "NoConvergence",
     "NonPositiveSpectrum",
+    "BadMagic",
+    "TruncatedPayload",
+    "DimMismatch",
     "ShapeMismatch",
     "BatchedMatrix",
     "BatchedSymmetric",
@@ -86,6 +89,18 @@ class NonPositiveSpectrum(BatchedEigError):
         )
         self.batch_index = batch_index
         self.min_eigenvalue = min_eigenvalue
+
+
+class BadMagic(BatchedEigError):
+    """Stream does not start with a supported BED1 header (core.py:67-68)."""
+
+
+class TruncatedPayload(BatchedEigError):
+    """Stream ended before the payload its header announced (core.py:71-72)."""
+
+
+class DimMismatch(BatchedEigError):
+    """Header dimensions are invalid or not the expected shape (core.py:75-76)."""
 
 
 class ShapeMismatch(BatchedEigError):
