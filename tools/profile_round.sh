@@ -13,5 +13,6 @@ done
 bash tools/ncu_export.sh bwd16 "bed_backward_kernel" 0 python tools/profile_cases.py 16
 bash tools/ncu_export.sh bwd64 "bed_backward_kernel" 0 python tools/profile_cases.py 64
 bash tools/ncu_export.sh pow16 "bed_power_kernel" 0 python tools/profile_cases.py 16 pow
+bash tools/ncu_export.sh scat16 "bed_scatter_kernel" 0 python tools/profile_cases.py scat
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv \
     python bench.py --steps 5 --warmup 3 --quick > gpurun_out/bench_under_ncu.json 2>&1
