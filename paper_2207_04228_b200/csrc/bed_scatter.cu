@@ -61,32 +61,23 @@ __global__ void __launch_bounds__(ScatParams<NMAX>::THREADS)
   const float* x = X + base * n * m;
   auto buf = [&](int mat) { return smem + mat * P::PER; };
 
-  // pass 1: channel means (warp per row, coalesced along samples)
-  for (int rr = warp; rr < P::MB * NMAX; rr += NWARP) {
-    const int mat = rr / NMAX, r = rr - mat * NMAX;
-    float s = 0.0f;
-    if (mat < count && r < n) {
-      const float* row = x + ((int64_t)mat * n + r) * m;
-      float s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
-      int k = lane;
-      for (; k + 96 < m; k += 128) {
-        s += __ldg(row + k);
-        s1 += __ldg(row + k + 32);
-        s2 += __ldg(row + k + 64);
-        s3 += __ldg(row + k + 96);
-      }
-      for (; k < m; k += 32) s += __ldg(row + k);
-      s += (s1 + s2) + s3;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) buf(mat)[KC * SROW + r] = (mat < count && r < n) ? s / (float)m : 0.0f;
+  // One pass over X, shifted by each channel's first sample x0 (which keeps
+  // the one-pass formula free of cancellation at the data's spread, not its
+  // offset):  S = sum_k (x_k - x0)(x_k - x0)^T - m d d^T,  d = mean(x - x0).
+  // The shift goes in the mean slot; the k-major chunks feed the 4 x 4
+  // FFMA2 tiles, and one thread per channel row sums its chunk column.
+  for (int g = tid; g < P::MB * NMAX; g += P::THREADS) {
+    const int mat = g / NMAX, r = g - mat * NMAX;
+    buf(mat)[KC * SROW + r] = (mat < count && r < n) ? __ldg(x + ((int64_t)mat * n + r) * m) : 0.0f;
   }
   __syncthreads();
-
-  // pass 2: S = X_c X_c^T over chunks of KC samples staged k-major
+  (void)lane;
+  (void)warp;
+  (void)NWARP;
   const int mi = tid / P::TPM, t = tid % P::TPM;
   const int ti = t / TQ, tj = t % TQ;
+  const int srow_mat = tid / NMAX, srow_r = tid % NMAX;  // row-sum owner (tid < MB * NMAX)
+  float rowsum = 0.0f;
   f2 acc[4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
@@ -102,8 +93,26 @@ __global__ void __launch_bounds__(ScatParams<NMAX>::THREADS)
       buf(mat)[k * SROW + r] = v;
     }
     __syncthreads();
+    if (tid < P::MB * NMAX) {
+      const float* col = buf(srow_mat) + srow_r;
+      for (int k = 0; k < kc; ++k) rowsum += col[k * SROW];
+    }
     tile_gemm_chunk<NMAX>(buf(mi), ti, tj, kc, acc);
     __syncthreads();
+  }
+  // d = rowsum / m into the stage row the chunks used (no longer needed)
+  if (tid < P::MB * NMAX) buf(srow_mat)[srow_r] = rowsum / (float)m;
+  __syncthreads();
+  {
+    const float* dv = buf(mi);
+    const float fm = (float)m;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const float di = dv[4 * ti + ii] * fm;
+#pragma unroll
+      for (int jp = 0; jp < 2; ++jp)
+        acc[ii][jp] = ffma2(f2_bc(-di), f2_make(dv[4 * tj + 2 * jp], dv[4 * tj + 2 * jp + 1]), acc[ii][jp]);
+    }
   }
   float* cs = buf(mi) + KC * SROW + NMAX;
 #pragma unroll
