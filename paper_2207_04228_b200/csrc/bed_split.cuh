@@ -230,12 +230,13 @@ __global__ void __launch_bounds__(kQThreads)
 // ---------------------------------------------------------------------------
 // F: fold the recorded rotations into V = P, then sort + sign + store.
 //
-// A CTA holds G matrices of ONE band warp (G divides 32), so all its groups
-// replay the same sweep sequence.  Each sweep's rotations for the CTA's
-// lanes ([position][lane] rows of G float2) are copied into shared memory
-// with coalesced loads one sweep ahead (register prefetch, double-buffered
-// shared buffer, one barrier per sweep); the groups then read their
-// rotation as a conflict-free broadcast.
+// A CTA holds G matrices of ONE band warp (G divides 32; small CTAs so the
+// load / fold / store phases of neighbouring CTAs overlap), so all its
+// groups replay the same sweep sequence.  The records are consumed in
+// phases of K sweeps (one barrier per phase), copied by cp.async into a
+// double-buffered, matrix-major shared buffer one phase ahead; each group
+// skips its own no-op sweeps and positions and reads two rotations per
+// 128-bit broadcast.
 template <int NMAX>
 struct FoldParams {
   static constexpr int L = GroupSize<NMAX>::L;
