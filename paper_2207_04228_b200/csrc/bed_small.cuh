@@ -260,16 +260,22 @@ __global__ void __launch_bounds__(kSmallThreads)
         for (int c = 0; c < N; ++c) x[r][c] = live ? my[r * N + c] : 0.0f;
     }
 
-    // ---- validate + symmetrise (core.py:286-309)
-    bool finite = true;
+    // ---- validate + symmetrise (core.py:286-309).  A NaN or Inf entry makes
+    // the square sum non-finite, so the per-entry scan runs only then (or
+    // when a finite entry's square overflows, where it finds nothing)
     float fro2 = 0.0f, asym = 0.0f;
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll
-      for (int c = 0; c < N; ++c) {
-        finite = finite && isfinite(x[r][c]);
-        fro2 = fmaf(x[r][c], x[r][c], fro2);
-      }
+      for (int c = 0; c < N; ++c) fro2 = fmaf(x[r][c], x[r][c], fro2);
+    bool finite = isfinite(fro2);
+    if (!finite) {
+      finite = true;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) finite = finite && isfinite(x[r][c]);
+    }
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll
