@@ -1,9 +1,9 @@
 // bed_hh.cuh -- H stage of the medium path (9 <= n <= 64): validation,
 // Householder tridiagonalisation and P = H_0 H_1 ... H_{n-3}.
 //
-// One warp (NMAX = 32, 64) or half-warp (NMAX = 16) owns a matrix; lane l
-// holds rows l and, for NMAX = 64, l + 32 of A in registers as packed column
-// pairs (bed_f32x2.cuh), so every p = A u product and every symmetric rank-2
+// A group of L lanes owns a matrix (4 lanes at n <= 16, 16 at n <= 32, two
+// warps at n = 64); lane l holds rows l, l + L, ... of A in registers as
+// packed column pairs (bed_f32x2.cuh), so every p = A u product and every symmetric rank-2
 // update runs as FFMA2 on two columns at once, with the reflector u and the
 // vector q read back from shared memory as 128-bit broadcasts.  All group
 // communication is warp shuffles -- no named barriers, no shared-memory
@@ -35,8 +35,9 @@ namespace bed {
 
 template <int NMAX>
 struct HHParams {
-  // n <= 32: two rows per lane (l and l + L): every shuffle reduction serves
-  // 32 / L matrices at once and each lane carries twice the FMA work.
+  // n <= 32: several rows per lane (l, l + L, ...; four at n <= 16, two at
+  // n <= 32): every shuffle reduction serves 32 / L matrices at once and each
+  // lane carries R times the FMA work between them.
   // n = 64: one row per lane over two warps (64 lanes), so a matrix needs
   // ~100 registers per thread instead of ~250 and twice the warps are in
   // flight; the two warps meet through shared memory and a named barrier.
