@@ -35,13 +35,13 @@ namespace bed {
 
 template <int NMAX>
 struct HHParams {
-  // n <= 32: several rows per lane (l, l + L, ...; four at n <= 16, two at
-  // n <= 32): every shuffle reduction serves 32 / L matrices at once and each
+  // n <= 32: several rows per lane (l, l + L, ...; four at n <= 16, three at
+  // n = 24, two at n <= 32): every shuffle reduction serves 32 / L matrices at once and each
   // lane carries R times the FMA work between them.
   // n = 64: one row per lane over two warps (64 lanes), so a matrix needs
   // ~100 registers per thread instead of ~250 and twice the warps are in
   // flight; the two warps meet through shared memory and a named barrier.
-  static constexpr int L = NMAX <= 16 ? 4 : (NMAX <= 32 ? 16 : 64);  // lanes per matrix
+  static constexpr int L = NMAX <= 16 ? 4 : (NMAX <= 24 ? 8 : (NMAX <= 32 ? 16 : 64));  // lanes per matrix
   static constexpr int R = (NMAX + L - 1) / L;                      // rows per lane
   static constexpr int MINB = 4;  // CTAs per SM the register cap must allow (128 registers)
   static constexpr int NP = NMAX / 2;              // column pairs per row
