@@ -10,12 +10,13 @@ import oracle  # noqa: E402
 import paper_2207_04228_b200 as bed  # noqa: E402
 
 torch.cuda.set_device(0)
-for n, b in ((3, 130), (4, 131), (8, 129), (9, 37), (16, 161), (24, 70), (32, 33), (40, 19), (64, 35)):
+for n, b in ((3, 130), (4, 131), (8, 129), (9, 37), (13, 41), (16, 161), (24, 70), (32, 33), (40, 19), (64, 35)):
     a = torch.from_numpy(oracle.gen_spd(b, n, n).astype(np.float32)).cuda().requires_grad_(True)
     lam, v = bed.eigh(a, bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n))
     (v.sum() + lam.sum()).backward()
     bed.batched_eig(a.detach(), bed.SolverConfig(compute_vectors=False, max_double_steps=4 * n))
     bed.matrix_power(bed.EigenResult(lam.detach(), v.detach(), None), -0.5)
+    bed.scatter_matrices(torch.randn(7, n, 2 * n + 3, device="cuda"), 1e-3)
 # chunked host path and a batch above the medium path's sub-warp tails
 x = oracle.gen_spd(3000, 4, 1).astype(np.float32)
 bed.batched_eig(x, bed.SolverConfig(deflation_tol=3e-12))
