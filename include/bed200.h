@@ -7,10 +7,13 @@
  * Plain pointers and sizes only.  Device entry points take device pointers
  * and a CUDA stream (cudaStream_t passed as void*), are asynchronous and
  * stream-ordered and reentrant (one call per device stream).  For n <= 8
- * they allocate nothing; for n >= 9 the forward takes a workspace (at most
- * 4 GiB or a quarter of free memory, reused chunk by chunk) from the device's stream-ordered memory pool
- * (cudaMallocAsync / cudaFreeAsync on the same stream).  The host entry
- * point takes host pointers and does the copies itself.
+ * nothing is allocated.  For n >= 9 the forward needs a device workspace:
+ * bed_forward_ws_f32 takes it from the caller (size from
+ * bed_forward_workspace_bytes; a smaller one solves the batch in chunks),
+ * bed_forward_f32 allocates it per call (at most 4 GiB, chunk by chunk) from
+ * a private stream-ordered pool of the library on the current device --
+ * the device's default pool is not touched.  The host entry point takes
+ * host pointers and does the copies itself.
  *
  * Reference interfaces each entry point replaces (paths relative to the
  * reference package root /root/reference/pkg/src/batchedeig):
@@ -25,6 +28,10 @@
  *                                                   householder.py:216-271
  *                          + V = P @ Q              solver.py:93
  *                          + _sort_and_sign         solver.py:60-76
+ *   bed_forward_ws_f32     the same, with a caller-owned workspace
+ *   bed_forward_workspace_bytes  its size (the reference preallocates
+ *                          its kernels' buffers in the caller the same way,
+ *                          householder.py:190-192, qr.py:601-602)
  *   bed_forward_host_f32   the same call on host (numpy-side) buffers, the
  *                          way the reference API is called (solver.py:79)
  *   bed_backward_f32       (absent in the reference: pkg/README.md:116-117)
@@ -41,13 +48,14 @@
 #ifndef BED200_H_
 #define BED200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define BED200_ABI_VERSION 1
+#define BED200_ABI_VERSION 2
 
 /* Return codes of every entry point. */
 #define BED_SUCCESS 0
@@ -64,7 +72,9 @@ extern "C" {
 #define BED_STATUS_NON_FINITE 2     /* NaN/Inf in the input matrix */
 #define BED_STATUS_NON_SYMMETRIC 3  /* max|a_ij-a_ji| > symmetry_tol * max(1, ||A||_F) */
 #define BED_STATUS_NON_POSITIVE 4   /* bed_matrix_power_f32: non-positive clamped eigenvalue
-                                       with a negative or fractional power (NonPositiveSpectrum) */
+                                       with a negative or fractional power (NonPositiveSpectrum);
+                                       bed_backward_f32: a pair outside the Taylor series'
+                                       domain (see there) */
 
 #define BED_SORT_NONE 0
 #define BED_SORT_DESCENDING 1
@@ -94,6 +104,22 @@ int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, floa
                     int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
                     void* stream);
 
+/* Bytes of device workspace bed_forward_ws_f32 needs to solve `batch`
+ * matrices of order n in one pass; 0 for n <= 8 (or batch <= 0).  The
+ * smallest workspace accepted is bed_forward_workspace_bytes(32, n, cfg):
+ * between the two, the batch is solved in chunks of whole multiples of 32.
+ * For 9 <= n <= 24 (and for values-only solves) it is 4 (n^2 + 2n + 1) bytes
+ * per matrix with vectors; for 25 <= n <= 64 with vectors it adds the
+ * rotation record of every sweep the double-step budget allows. */
+size_t bed_forward_workspace_bytes(int64_t batch, int32_t n, const bed_config* cfg);
+
+/* bed_forward_f32 with a caller-owned device workspace (256-byte aligned,
+ * ignored for n <= 8).  No allocation inside.  BED_ERR_INVALID_ARGUMENT if
+ * it is smaller than bed_forward_workspace_bytes(32, n, cfg). */
+int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
+                       int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* Same computation on HOST buffers (pinned or pageable), on CUDA device
  * `device`.  Streams the batch through the GPU in chunks with copies
  * overlapped against compute; returns after the results are on the host. */
@@ -103,10 +129,16 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
 /* Backward with the Taylor-polynomial K of degree `taylor_degree` (paper: 9):
  *   gA = sym( V (F o (V^T gV) + diag(gL)) V^T ),  sym(M) = (M + M^T)/2,
  *   F_ij ~ 1/(l_j - l_i) via (1/l_big) sum_{k=0..degree} (l_small/l_big)^k.
+ * The series is the paper's for positive spectra (covariance inputs).  A pair
+ * outside its domain -- l_big <= 0, or l_small <= -l_big (|ratio| >= 1 and not
+ * a tie) -- takes the exact 1/(l_j - l_i) instead, and the matrix's status is
+ * BED_STATUS_NON_POSITIVE (bit 1 << 4 in flags).  Two zero eigenvalues give 0.
  * V (batch,n,n), evals (batch,n) as returned by bed_forward_f32; gV and gL
- * are nullable (zero cotangent); gA (batch,n,n) is written. Device pointers. */
+ * are nullable (zero cotangent); gA (batch,n,n) is written; status (batch)
+ * and flags (1) are nullable.  Device pointers, stream-ordered. */
 int bed_backward_f32(const float* V, const float* evals, const float* gV, const float* gL,
-                     float* gA, int64_t batch, int32_t n, int32_t taylor_degree, void* stream);
+                     float* gA, int64_t batch, int32_t n, int32_t taylor_degree, int32_t* status,
+                     int32_t* flags, void* stream);
 
 /* Spectral power  out = sym( V diag(max(evals, floor)^p) V^T )  of a decomposed
  * batch (reference matrix_power, solver.py:115-143).  floor < 0 selects the

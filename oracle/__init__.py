@@ -14,7 +14,9 @@ Contents
                        The reference package has no backward
                        (``pkg/README.md:116-117``): **parity unpinned** against
                        the reference; pinned instead by the known-answer
-                       properties in ``tests/test_oracle_backward.py``.
+                       properties in ``tests/test_oracle_backward.py`` (SURVEY.md 8(c)
+                       (i)-(v), including degree -> inf against float64
+                       ``torch.linalg.eigh`` autograd).
 ``matrix_power``       float64 restatement of the reference spectral power
                        (``solver.py:115-143``), the checker of
                        ``bed_matrix_power_f32``.
@@ -32,6 +34,7 @@ from .oracle import (  # noqa: F401
     library_path,
     matrix_power,
     taylor_backward,
+    taylor_domain,
     taylor_k,
     wilkinson,
     tridiagonalize,

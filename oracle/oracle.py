@@ -147,9 +147,16 @@ def taylor_k(evals, degree: int = 9) -> np.ndarray:
 
     For a pair i < j with lambda_i >= lambda_j (descending order, ties by
     index) F_ij = -(1/lambda_i) * sum_{k=0..degree} (lambda_j/lambda_i)^k and
-    F_ji = -F_ij; if lambda_i < lambda_j the roles swap.  F_ii = 0.  A zero
-    larger eigenvalue gives F = 0.  Paper: PAPER.md:668 (backward reuses
-    [song2021approximate]), PAPER.md:700 (Taylor degree 9).
+    F_ji = -F_ij; if lambda_i < lambda_j the roles swap.  F_ii = 0.  Paper:
+    PAPER.md:668 (backward reuses [song2021approximate])
+    (Taylor degree 9).
+
+    The series sums to 1/(l_big - l_small) only for |l_small/l_big| < 1 (and
+    is (degree+1)/l on ties): the positive spectra the paper's covariance
+    inputs have.  A pair outside that domain (l_big <= 0, or l_small <=
+    -l_big, not a tie) takes the exact 1/(lambda_j - lambda_i); two zero
+    eigenvalues, or a tie outside the domain, give F = 0.  :func:`taylor_domain` reports which matrices
+    had such a pair (the kernel's BED_STATUS_NON_POSITIVE).
     """
     lam = np.asarray(evals, dtype=np.float64)
     b, n = lam.shape
@@ -164,15 +171,35 @@ def taylor_k(evals, degree: int = 9) -> np.ndarray:
     with np.errstate(divide="ignore", invalid="ignore"):
         ratio = np.where(big != 0, small / np.where(big != 0, big, 1.0), 0.0)
         inv = np.where(big != 0, 1.0 / np.where(big != 0, big, 1.0), 0.0)
+        gap = big - small
+        exact = np.where(gap != 0, 1.0 / np.where(gap != 0, gap, 1.0), 0.0)
     acc = np.ones_like(ratio)
     term = np.ones_like(ratio)
     for _ in range(degree):
         term = term * ratio
         acc = acc + term
-    t = inv * acc
+    t = np.where(_in_domain(big, small, ratio), inv * acc, exact)
     f = np.where(hi_first, -t, t)
     f[:, idx, idx] = 0.0
     return f
+
+
+def _in_domain(big, small, ratio):
+    return ((big > 0) & ((np.abs(ratio) < 1) | (small == big))) | ((big == 0) & (small == 0))
+
+
+def taylor_domain(evals) -> np.ndarray:
+    """True per matrix when every eigenvalue pair is inside the Taylor
+    series' domain (see :func:`taylor_k`)."""
+    lam = np.asarray(evals, dtype=np.float64)
+    li, lj = lam[:, :, None], lam[:, None, :]
+    big, small = np.maximum(li, lj), np.minimum(li, lj)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = np.where(big != 0, small / np.where(big != 0, big, 1.0), 0.0)
+    ok = _in_domain(big, small, ratio)
+    n = lam.shape[1]
+    ok[:, np.arange(n), np.arange(n)] = True
+    return ok.all(axis=(1, 2))
 
 
 def taylor_backward(v, evals, g_v=None, g_evals=None, degree: int = 9) -> np.ndarray:

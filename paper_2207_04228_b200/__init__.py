@@ -32,9 +32,16 @@ from .solver import (  # noqa: F401
     matrix_power,
     scatter_matrices,
     taylor_backward,
+    workspace,
     zca_whiten,
 )
 from .bed_io import read_batch, read_matrix, write_batch  # noqa: F401
-from .sharding import gather_shards, shard_bounds, shard_sizes, solve_shard  # noqa: F401
+from .sharding import (  # noqa: F401
+    batched_eig_devices,
+    gather_shards,
+    shard_bounds,
+    shard_sizes,
+    solve_shard,
+)
 
 __version__ = "0.1.0"

@@ -23,6 +23,8 @@ STATUS_NON_POSITIVE = 4
 # every symbol include/bed200.h declares
 EXPORTS = (
     "bed_forward_f32",
+    "bed_forward_ws_f32",
+    "bed_forward_workspace_bytes",
     "bed_forward_host_f32",
     "bed_backward_f32",
     "bed_matrix_power_f32",
@@ -68,10 +70,15 @@ def lib() -> ctypes.CDLL:
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     L.bed_forward_f32.restype = ctypes.c_int
     L.bed_forward_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, ctypes.POINTER(BedConfig), vp]
+    L.bed_forward_ws_f32.restype = ctypes.c_int
+    L.bed_forward_ws_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, ctypes.POINTER(BedConfig),
+                                     vp, ctypes.c_size_t, vp]
+    L.bed_forward_workspace_bytes.restype = ctypes.c_size_t
+    L.bed_forward_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(BedConfig)]
     L.bed_forward_host_f32.restype = ctypes.c_int
     L.bed_forward_host_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, ctypes.POINTER(BedConfig), i32]
     L.bed_backward_f32.restype = ctypes.c_int
-    L.bed_backward_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, i32, vp]
+    L.bed_backward_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, i32, vp, vp, vp]
     L.bed_matrix_power_f32.restype = ctypes.c_int
     L.bed_matrix_power_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, ctypes.c_float,
                                        ctypes.c_float, vp]
@@ -114,8 +121,21 @@ def forward_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr, fl
     check(rc, "bed_forward_f32")
 
 
-def backward_f32(V_ptr, evals_ptr, gV_ptr, gL_ptr, gA_ptr, batch, n, degree, stream) -> None:
-    rc = lib().bed_backward_f32(V_ptr, evals_ptr, gV_ptr, gL_ptr, gA_ptr, batch, n, degree, stream)
+def forward_ws_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr, flags_ptr,
+                   cfg: BedConfig, ws_ptr, ws_bytes: int, stream: int) -> None:
+    rc = lib().bed_forward_ws_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr,
+                                  flags_ptr, ctypes.byref(cfg), ws_ptr, ws_bytes, stream)
+    check(rc, "bed_forward_ws_f32")
+
+
+def workspace_bytes(batch: int, n: int, cfg: BedConfig) -> int:
+    return int(lib().bed_forward_workspace_bytes(batch, n, ctypes.byref(cfg)))
+
+
+def backward_f32(V_ptr, evals_ptr, gV_ptr, gL_ptr, gA_ptr, batch, n, degree, status_ptr,
+                 flags_ptr, stream) -> None:
+    rc = lib().bed_backward_f32(V_ptr, evals_ptr, gV_ptr, gL_ptr, gA_ptr, batch, n, degree,
+                                status_ptr, flags_ptr, stream)
     check(rc, "bed_backward_f32")
 
 

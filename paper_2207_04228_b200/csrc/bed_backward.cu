@@ -8,16 +8,10 @@ template <int NMAX, bool EXACT>
 static cudaError_t go_bwd(const BwdArgs& a) {
   using P = BwdParams<NMAX>;
   auto kern = bed_backward_kernel<NMAX, EXACT>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P::BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem(kern, P::BYTES); e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.batch + P::MB - 1) / P::MB);
   kern<<<grid, P::THREADS, P::BYTES, a.stream>>>(a.V, a.lam, a.gV, a.gL, a.gA, a.batch, a.n,
-                                                 a.degree);
+                                                 a.degree, a.status, a.flags);
   return cudaGetLastError();
 }
 

@@ -4,6 +4,12 @@
 //   F_ij ~ 1/(l_j - l_i):  for the pair's larger value l_big (index order on
 //   ties) and smaller l_small,  T = (1/l_big) sum_{k=0..K} (l_small/l_big)^k,
 //   F_ij = -T when l_i is the larger, +T otherwise; F_ii = 0.
+// The series converges to 1/(l_j - l_i) only for |l_small / l_big| < 1 (and
+// equals (K+1)/l on ties), i.e. on the positive spectra of the paper's
+// covariance inputs.  A pair outside that domain
+// (l_big <= 0, or l_small <= -l_big) takes the exact 1/(l_j - l_i) instead
+// and its matrix is reported as BED_STATUS_NON_POSITIVE (a pair of zeros,
+// or a tie outside the domain, gives F = 0).
 //
 // The reference package has no backward (pkg/README.md:116-117); the paper
 // reuses [song2021approximate] with a degree-9 Taylor polynomial
@@ -69,7 +75,8 @@ template <int NMAX, bool EXACT>
 __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
     bed_backward_kernel(const float* __restrict__ V, const float* __restrict__ lam,
                         const float* __restrict__ gV, const float* __restrict__ gL,
-                        float* __restrict__ gA, int64_t batch, int n_rt, int degree) {
+                        float* __restrict__ gA, int64_t batch, int n_rt, int degree,
+                        int32_t* __restrict__ status_out, int32_t* __restrict__ flags) {
   using P = BwdParams<NMAX>;
   constexpr int SROW = P::SROW, TQ = P::TQ;
   const int n = EXACT ? NMAX : n_rt;
@@ -86,6 +93,7 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
   float* sX = sT + P::SBUF;        // gV -> M' -> G
   float* sL = sX + P::SBUF;
   float* sI = sL + NMAX;
+  __shared__ int outside[P::MB];  // matrix has a pair outside the Taylor domain
 
   if (!EXACT) {  // padding rows/columns must read as zeros in the products
     for (int g = tid; g < P::MB * P::PER; g += P::THREADS) smem[g] = 0.0f;
@@ -103,6 +111,7 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
     dl[NMAX + c] = l != 0.0f ? 1.0f / l : 0.0f;
   }
   __syncthreads();
+  for (int g = tid; g < P::MB; g += P::THREADS) outside[g] = 0;
   // V^T from V
   for (int g = tid; g < P::MB * NMAX * NMAX; g += P::THREADS) {
     const int mat = g / (NMAX * NMAX), off = g - mat * NMAX * NMAX;
@@ -120,6 +129,13 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
   if (gV) tile_gemm<NMAX, SROW>(sV, sX, ti, tj, acc);
   // F by Horner in packed pairs (two tile columns per FFMA2)
   float mp[4][4];
+  bool off_domain = false;
+  // a tile whose eight eigenvalues are all positive is inside the series'
+  // domain (0 < l_small <= l_big): no per-pair check
+  float tmin = sL[4 * ti];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tmin = fminf(tmin, fminf(sL[4 * ti + q], sL[4 * tj + q]));
+  const bool tile_pos = tmin > 0.0f;
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) {
     const int i = 4 * ti + ii;
@@ -144,13 +160,30 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int jj = 2 * jp + h, j = 4 * tj + jj;
-        const float tv = h ? f2_hi(tt) : f2_lo(tt);
+        float tv = h ? f2_hi(tt) : f2_lo(tt);
+        if (!tile_pos) {
+          // the series' domain: l_big > 0 and |ratio| < 1, or a tie (ratio 1)
+          const float lj = sL[j];
+          const float big = hf[h] ? li : lj, small = hf[h] ? lj : li;
+          const bool in_domain = (big > 0.0f && (fabsf(ratio[h]) < 1.0f || small == big)) ||
+                                 (big == 0.0f && small == 0.0f);
+          if (!in_domain && i != j && i < n && j < n) {
+            tv = big != small ? 1.0f / (big - small) : 0.0f;  // exact 1/(l_j - l_i), sign below
+            off_domain = true;
+          }
+        }
         const float f = i == j ? 0.0f : (hf[h] ? -tv : tv);
         mp[ii][jj] = f * tile_at(acc, ii, jj) + (i == j ? gli : 0.0f);
       }
     }
   }
+  if (off_domain && live) atomicOr(&outside[mi], 1);
   __syncthreads();  // every thread is done reading gV
+  if (t == 0 && live) {
+    const int st = outside[mi] ? kStatusNonPositive : kStatusOk;
+    if (status_out) status_out[base + mi] = st;
+    if (flags && st) atomicOr(flags, 1 << st);
+  }
   if (live) {
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)

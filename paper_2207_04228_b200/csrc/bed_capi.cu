@@ -8,9 +8,11 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "../../include/bed200.h"
 #include "bed_launch.h"
+#include "bed_split_plan.h"
 
 namespace {
 
@@ -51,19 +53,38 @@ bed::KernelCfg kernel_cfg(const bed_config* cfg, int n) {
   return k;
 }
 
-// The n >= 9 path takes its workspace from the device's stream-ordered
-// memory pool; keep freed blocks cached in the pool across calls.
-void keep_pool_warm() {
-  static bool done[64] = {};
+// Device memory the library allocates itself (the n >= 9 workspace of
+// bed_forward_f32, the slot buffers of bed_forward_host_f32) comes from a
+// private stream-ordered pool per device that keeps freed blocks cached --
+// the device's default pool and its settings are left alone.  Callers that
+// want their own allocator to own the memory use bed_forward_ws_f32.
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      if ((e = cudaMemPoolCreate(&pools[dev], &props)) != cudaSuccess) return e;
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = pools[dev];
   }
-  done[dev] = true;
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
+
+// Workspace bed_forward_f32 allocates per call: the whole batch in one chunk
+// up to 4 GiB, chunked beyond; halved while the pool refuses.
+constexpr size_t kWorkspaceCap = size_t(4) << 30;
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -78,14 +99,35 @@ int64_t host_chunk_bytes() {
 }
 
 cudaError_t dispatch_forward(const bed::FwdArgs& a) {
-  if (a.n > 8) keep_pool_warm();
   if (a.n <= 8) return bed::launch_small(a);
   if (a.n <= 16) return bed::launch_split16(a);
+  if (a.n <= 24) return bed::launch_split24(a);
   if (a.n <= 32) return bed::launch_split32(a);
   return bed::launch_split64(a);
 }
 
 }  // namespace
+
+namespace bed {
+
+cudaError_t ensure_smem(const void* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  struct Entry { const void* fn; int dev; };
+  static std::mutex mu;
+  static Entry done[512];
+  static int ndone = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i].fn == kern && done[i].dev == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && ndone < 512) done[ndone++] = Entry{kern, dev};
+  return e;
+}
+
+}  // namespace bed
 
 extern "C" {
 
@@ -104,32 +146,79 @@ const char* bed_error_string(int code) {
 
 const char* bed_last_cuda_error(void) { return g_last_cuda; }
 
+size_t bed_forward_workspace_bytes(int64_t batch, int32_t n, const bed_config* cfg) {
+  if (!cfg || batch <= 0 || n <= 8 || n > 64) return 0;
+  const bed::KernelCfg k = kernel_cfg(cfg, n);
+  return bed::split_plan((batch + 31) / 32 * 32, n, cfg->compute_vectors != 0, k.max_steps).bytes;
+}
+
+int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
+                       int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_forward(A, batch, n, evals, evecs, cfg);
+  if (rc) return rc;
+  const bool vecs = cfg->compute_vectors != 0;
+  const bed::KernelCfg k = kernel_cfg(cfg, n);
+  if (batch > 0 && n > 8 &&
+      (!workspace || bed::split_chunk(batch, n, vecs, k.max_steps, workspace_bytes) == 0))
+    return BED_ERR_INVALID_ARGUMENT;  // below bed_forward_workspace_bytes(32, n, cfg)
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0) return BED_ERR_MISALIGNED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags) {
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "bed_forward_ws_f32 memset(flags)");
+  }
+  if (batch == 0) return BED_SUCCESS;
+  bed::FwdArgs a{A, batch, n, evals, vecs ? evecs : nullptr, status, steps, flags, k, s,
+                 workspace, workspace_bytes};
+  cudaError_t e = dispatch_forward(a);
+  if (e != cudaSuccess) return cuda_fail(e, "bed_forward_ws_f32 launch");
+  return BED_SUCCESS;
+}
+
 int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
                     int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
                     void* stream) {
   int rc = check_forward(A, batch, n, evals, evecs, cfg);
   if (rc) return rc;
+  if (batch == 0 || n <= 8)
+    return bed_forward_ws_f32(A, batch, n, evals, evecs, status, steps, flags, cfg, nullptr, 0,
+                              stream);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (flags) {
-    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
-    if (e != cudaSuccess) return cuda_fail(e, "bed_forward_f32 memset(flags)");
+  const bool vecs = cfg->compute_vectors != 0;
+  const int max_steps = kernel_cfg(cfg, n).max_steps;
+  size_t bytes = std::min(bed_forward_workspace_bytes(batch, n, cfg), kWorkspaceCap);
+  const size_t floor_bytes = bed::split_plan(32, n, vecs, max_steps).bytes;
+  bytes = std::max(bytes, floor_bytes);
+  void* ws = nullptr;
+  cudaError_t e = pool_alloc(&ws, bytes, s);
+  while (e == cudaErrorMemoryAllocation && bytes > floor_bytes) {
+    cudaGetLastError();  // clear the allocation error and retry smaller
+    bytes = std::max(floor_bytes, bytes / 2);
+    e = pool_alloc(&ws, bytes, s);
   }
-  if (batch == 0) return BED_SUCCESS;
-  bed::FwdArgs a{A, batch, n, evals, cfg->compute_vectors ? evecs : nullptr, status, steps,
-                 flags, kernel_cfg(cfg, n), s};
-  cudaError_t e = dispatch_forward(a);
-  if (e != cudaSuccess) return cuda_fail(e, "bed_forward_f32 launch");
-  return BED_SUCCESS;
+  if (e != cudaSuccess) return cuda_fail(e, "bed_forward_f32 workspace");
+  rc = bed_forward_ws_f32(A, batch, n, evals, evecs, status, steps, flags, cfg, ws, bytes, stream);
+  e = cudaFreeAsync(ws, s);
+  if (rc == BED_SUCCESS && e != cudaSuccess) return cuda_fail(e, "bed_forward_f32 free");
+  return rc;
 }
 
 int bed_backward_f32(const float* V, const float* evals, const float* gV, const float* gL,
-                     float* gA, int64_t batch, int32_t n, int32_t taylor_degree, void* stream) {
+                     float* gA, int64_t batch, int32_t n, int32_t taylor_degree, int32_t* status,
+                     int32_t* flags, void* stream) {
   if (batch < 0 || n < 1 || n > 64 || taylor_degree < 0) return BED_ERR_INVALID_ARGUMENT;
   if (batch > 0 && (!V || !evals || !gA)) return BED_ERR_INVALID_ARGUMENT;
-  if (!aligned4(V) || !aligned4(evals) || !aligned4(gV) || !aligned4(gL) || !aligned4(gA))
+  if (!aligned4(V) || !aligned4(evals) || !aligned4(gV) || !aligned4(gL) || !aligned4(gA) ||
+      !aligned4(status) || !aligned4(flags))
     return BED_ERR_MISALIGNED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags) {
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "bed_backward_f32 memset(flags)");
+  }
   if (batch == 0) return BED_SUCCESS;
-  bed::BwdArgs a{V, evals, gV, gL, gA, batch, n, taylor_degree, static_cast<cudaStream_t>(stream)};
+  bed::BwdArgs a{V, evals, gV, gL, gA, batch, n, taylor_degree, status, flags, s};
   cudaError_t e = bed::launch_backward(a);
   if (e != cudaSuccess) return cuda_fail(e, "bed_backward_f32 launch");
   return BED_SUCCESS;
@@ -187,7 +276,6 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
 
-  keep_pool_warm();  // the slot buffers come back from the pool on the next call
   const bool vecs = cfg->compute_vectors != 0;
   const int64_t nn = (int64_t)n * n;
   const int64_t per = 4 * (nn + n + (vecs ? nn : 0)) + 8;  // bytes in flight per matrix
@@ -206,7 +294,8 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
     for (int b = 0; b < kSlots && out == BED_SUCCESS; ++b)
       if ((e = cudaEventCreateWithFlags(&ev[r][b], cudaEventDisableTiming)) != cudaSuccess) out = cuda_fail(e, "event");
   }
-  if (out == BED_SUCCESS && (e = cudaMallocAsync(reinterpret_cast<void**>(&pool), slot * kSlots, st[C])) != cudaSuccess)
+  const size_t wsb = n > 8 ? std::max(bed_forward_workspace_bytes(chunk, n, cfg), (size_t)0) : 0;
+  if (out == BED_SUCCESS && (e = pool_alloc(reinterpret_cast<void**>(&pool), slot * kSlots + wsb, st[C])) != cudaSuccess)
     out = cuda_fail(e, "bed_forward_host_f32 allocation");
   if (out == BED_SUCCESS && (e = cudaEventRecord(ev[C][0], st[C])) == cudaSuccess) {
     // the H2D stream must not touch the pool before it is allocated
@@ -230,7 +319,8 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
     // solve: after this chunk's input arrived and slot b's outputs were read back
     if ((e = cudaStreamWaitEvent(st[C], ev[H][b], 0)) != cudaSuccess ||
         (used[b] && (e = cudaStreamWaitEvent(st[C], ev[D][b], 0)) != cudaSuccess)) { out = cuda_fail(e, "wait"); break; }
-    bed::FwdArgs a{dA, m, n, dL, dV, dS, dK, nullptr, kernel_cfg(cfg, n), st[C]};
+    bed::FwdArgs a{dA, m, n, dL, dV, dS, dK, nullptr, kernel_cfg(cfg, n), st[C],
+                   wsb ? pool + slot * kSlots : nullptr, wsb};
     if ((e = dispatch_forward(a)) != cudaSuccess) { out = cuda_fail(e, "bed_forward_host_f32 launch"); break; }
     if ((e = cudaEventRecord(ev[C][b], st[C])) != cudaSuccess) { out = cuda_fail(e, "record"); break; }
     // D2H

@@ -25,6 +25,7 @@ constexpr int kStatusOk = 0;
 constexpr int kStatusNoConv = 1;
 constexpr int kStatusNonFinite = 2;
 constexpr int kStatusNonSym = 3;
+constexpr int kStatusNonPositive = 4;
 
 // Column tails at or below this are already reduced (householder.py:37-39
 // uses 1e-300 in float64; this is the FP32 analogue, well above the

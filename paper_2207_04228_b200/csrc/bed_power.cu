@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(PowParams<NMAX>::THREADS)
       sf[c] = x;
     }
     for (int c = 0; c < n; ++c) sf[c] = bad ? 0.0f : spectral_pow(sf[c], p);
-    if (status) status[base + mi] = bad ? 4 : 0;
-    if (bad && flags) atomicOr(flags, 1 << 4);
+    if (status) status[base + mi] = bad ? kStatusNonPositive : kStatusOk;
+    if (bad && flags) atomicOr(flags, 1 << kStatusNonPositive);
   }
   __syncthreads();
   // V^T and diag(f) V^T from V
@@ -117,13 +117,7 @@ template <int NMAX, bool EXACT>
 static cudaError_t go_pow(const PowArgs& a) {
   using P = PowParams<NMAX>;
   auto kern = bed_power_kernel<NMAX, EXACT>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P::BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem(kern, P::BYTES); e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.batch + P::MB - 1) / P::MB);
   kern<<<grid, P::THREADS, P::BYTES, a.stream>>>(a.V, a.lam, a.out, a.status, a.flags, a.batch,
                                                  a.n, a.p, a.floor_abs, a.needs_positive);

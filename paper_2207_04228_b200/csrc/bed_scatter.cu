@@ -22,6 +22,8 @@ struct ScatParams {
   static constexpr int MB = TPM >= 128 ? 1 : 128 / TPM;  // matrices per CTA
   static constexpr int THREADS = MB * TPM;
   static constexpr int KC = 32;                         // samples per staged chunk
+  static constexpr int ROWS = MB * NMAX;                // (matrix, channel) row-sum owners
+  static constexpr int RPT = (ROWS + THREADS - 1) / THREADS;  // owners per thread
   static constexpr int SROW = NMAX + 4;
   static constexpr int PER = KC * SROW + NMAX + NMAX * (NMAX + 1);  // X_c^T chunk, mu, result
   static constexpr size_t BYTES = sizeof(float) * (size_t)MB * PER;
@@ -76,8 +78,11 @@ __global__ void __launch_bounds__(ScatParams<NMAX>::THREADS)
   (void)NWARP;
   const int mi = tid / P::TPM, t = tid % P::TPM;
   const int ti = t / TQ, tj = t % TQ;
-  const int srow_mat = tid / NMAX, srow_r = tid % NMAX;  // row-sum owner (tid < MB * NMAX)
-  float rowsum = 0.0f;
+  // Row-sum owners: (matrix, channel) pairs o = tid + q * THREADS, strided
+  // so every pair of the CTA has one (ROWS can exceed THREADS for n <= 8).
+  float rowsum[P::RPT];
+#pragma unroll
+  for (int q = 0; q < P::RPT; ++q) rowsum[q] = 0.0f;
   f2 acc[4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
@@ -93,15 +98,23 @@ __global__ void __launch_bounds__(ScatParams<NMAX>::THREADS)
       buf(mat)[k * SROW + r] = v;
     }
     __syncthreads();
-    if (tid < P::MB * NMAX) {
-      const float* col = buf(srow_mat) + srow_r;
-      for (int k = 0; k < kc; ++k) rowsum += col[k * SROW];
+#pragma unroll
+    for (int q = 0; q < P::RPT; ++q) {
+      const int o = tid + q * P::THREADS;
+      if (o < P::ROWS) {
+        const float* col = buf(o / NMAX) + o % NMAX;
+        for (int k = 0; k < kc; ++k) rowsum[q] += col[k * SROW];
+      }
     }
     tile_gemm_chunk<NMAX>(buf(mi), ti, tj, kc, acc);
     __syncthreads();
   }
   // d = rowsum / m into the stage row the chunks used (no longer needed)
-  if (tid < P::MB * NMAX) buf(srow_mat)[srow_r] = rowsum / (float)m;
+#pragma unroll
+  for (int q = 0; q < P::RPT; ++q) {
+    const int o = tid + q * P::THREADS;
+    if (o < P::ROWS) buf(o / NMAX)[o % NMAX] = rowsum[q] / (float)m;
+  }
   __syncthreads();
   {
     const float* dv = buf(mi);
@@ -135,13 +148,7 @@ template <int NMAX>
 static cudaError_t go_scatter(const ScatArgs& a) {
   using P = ScatParams<NMAX>;
   auto kern = bed_scatter_kernel<NMAX>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P::BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem(kern, P::BYTES); e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.batch + P::MB - 1) / P::MB);
   kern<<<grid, P::THREADS, P::BYTES, a.stream>>>(a.X, a.out, a.batch, a.n, a.m, a.eps);
   return cudaGetLastError();

@@ -46,8 +46,8 @@ namespace bed {
 // code over all NMAX positions (rotations past a lane's block are exact
 // identities; m = 0 is a no-op); positions no lane of the warp needs are
 // skipped by a vote.  Returns the warp's processed extent.  With VECS every
-// rotation is stored to rec[p * 32].
-template <int NMAX, bool VECS>
+// rotation is stored to rec[p * RSTRIDE].
+template <int NMAX, bool VECS, int RSTRIDE = 32>
 __device__ __forceinline__ int qr_sweep(float (&d)[NMAX], float (&e)[NMAX], int m, float mu,
                                         float2* __restrict__ rec) {
   float dw = d[0] - mu, g = e[0];
@@ -63,7 +63,7 @@ __device__ __forceinline__ int qr_sweep(float (&d)[NMAX], float (&e)[NMAX], int 
     const float ei = (i < NMAX - 1 && act) ? e[i] : 0.0f;
     float c, s, r;
     givens(dw, ei, c, s, r);
-    if (VECS && i < NMAX - 1) rec[i * 32] = make_float2(c, s);
+    if (VECS && i < NMAX - 1) rec[i * RSTRIDE] = make_float2(c, s);
     const float dn = (i + 1 < NMAX ? d[i + 1] : 0.0f) - mu;
     // (u, dw') = (c g - s dn, s g + c dn): one FMUL2 + one FFMA2
     const f2 ud = ffma2(f2_make(-s, c), f2_bc(dn), fmul2(f2_make(c, s), f2_bc(g)));

@@ -19,7 +19,7 @@ import torch.distributed as dist
 
 from .core import SolverConfig
 
-__all__ = ["shard_bounds", "shard_sizes", "solve_shard", "gather_shards"]
+__all__ = ["shard_bounds", "shard_sizes", "solve_shard", "gather_shards", "batched_eig_devices"]
 
 
 def shard_sizes(batch: int, world: int) -> list[int]:
@@ -85,3 +85,73 @@ def gather_shards(local: torch.Tensor, batch: int, group=None) -> torch.Tensor:
     out = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(out, pad, group=group)
     return torch.cat([o[:s] for o, s in zip(out, sizes)], dim=0)
+
+
+def batched_eig_devices(a: torch.Tensor, cfg: SolverConfig | None = None,
+                        devices: list[int] | None = None, out_device: int | str | None = None):
+    """Single-process sharding: the batch is cut into ``len(devices)``
+    contiguous slices (:func:`shard_bounds`), each solved on its own device
+    and CUDA stream -- the H2D copy of the slice, the solve and the copy of
+    its results into the output run on that stream, so the devices (or, with
+    a device listed twice, two streams of one device) work concurrently.  No
+    collective: every matrix is independent (per-matrix deflation).
+
+    ``a`` is a (batch, n, n) float32 tensor on any device or the host (pin
+    it for asynchronous copies).  Results land on ``out_device`` (default:
+    the first listed device) and are bit-identical to one
+    ``batched_eig`` call on the whole batch.  Raises like ``batched_eig``.
+    """
+    from . import solver
+    from .core import EigenResult
+
+    cfg = cfg or SolverConfig()
+    devices = list(range(torch.cuda.device_count())) if devices is None else list(devices)
+    if not devices:
+        raise RuntimeError("batched_eig_devices needs at least one CUDA device")
+    if a.ndim != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError(f"expected (batch, n, n), got {tuple(a.shape)}")
+    b, n, _ = a.shape
+    out_dev = torch.device("cuda", devices[0]) if out_device is None else torch.device(out_device)
+    evals = torch.empty((b, n), device=out_dev, dtype=torch.float32)
+    evecs = torch.empty((b, n, n), device=out_dev, dtype=torch.float32) if cfg.compute_vectors else None
+    status = torch.empty((b,), device=out_dev, dtype=torch.int32)
+    steps = torch.empty((b,), device=out_dev, dtype=torch.int32)
+    producer = torch.cuda.current_stream(a.device) if a.is_cuda else None
+    consumer = torch.cuda.current_stream(out_dev) if out_dev.type == "cuda" else None
+    streams = []
+    for r, d in enumerate(devices):
+        lo, hi = shard_bounds(b, len(devices), r)
+        if hi <= lo:
+            continue
+        dev = torch.device("cuda", d)
+        st = torch.cuda.Stream(dev)
+        streams.append(st)
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            if producer is not None:
+                st.wait_stream(producer)
+            local = a[lo:hi].to(dev, non_blocking=True).contiguous()
+            if consumer is not None:
+                st.wait_stream(consumer)  # the output buffers are ready
+            le = torch.empty((hi - lo, n), device=dev, dtype=torch.float32)
+            lv = torch.empty((hi - lo, n, n), device=dev, dtype=torch.float32) if evecs is not None else None
+            ls = torch.empty((hi - lo,), device=dev, dtype=torch.int32)
+            lk = torch.empty((hi - lo,), device=dev, dtype=torch.int32)
+            solver.forward_into(local, cfg, le, lv, ls, lk)
+            evals[lo:hi].copy_(le, non_blocking=True)
+            if lv is not None:
+                evecs[lo:hi].copy_(lv, non_blocking=True)
+            status[lo:hi].copy_(ls, non_blocking=True)
+            steps[lo:hi].copy_(lk, non_blocking=True)
+            for t in (evals, evecs, status, steps):
+                if t is not None and t.is_cuda:
+                    t.record_stream(st)
+    for st in streams:
+        if consumer is not None:
+            consumer.wait_stream(st)
+        else:
+            st.synchronize()
+    flags = 0
+    for code in torch.unique(status.cpu()).tolist():
+        flags |= (1 << code) if code else 0
+    solver._raise_for_status(a, status, flags, cfg)
+    return EigenResult(evals, evecs, solver._diagnostics(steps))

@@ -29,7 +29,7 @@ from .core import (
     SolverConfig,
 )
 
-__all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into",
+__all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into", "workspace",
            "matrix_power", "zca_whiten", "scatter_matrices", "TAYLOR_DEGREE"]
 
 TAYLOR_DEGREE = 9
@@ -47,17 +47,40 @@ def _check_cuda_f32(t: torch.Tensor, name: str) -> torch.Tensor:
     return t.contiguous()
 
 
+def workspace(A: torch.Tensor, cfg: SolverConfig, max_bytes: int | None = None) -> torch.Tensor | None:
+    """A device workspace for ``forward_into`` from torch's caching allocator
+    (``bed_forward_workspace_bytes``; None for n <= 8).  ``max_bytes`` caps it,
+    in which case the batch is solved in chunks."""
+    b, n, _ = A.shape
+    c = _native.make_config(cfg, n)
+    need = _native.workspace_bytes(b, n, c)
+    if need == 0:
+        return None
+    if max_bytes is not None:
+        need = max(min(need, int(max_bytes)), _native.workspace_bytes(32, n, c))
+    return torch.empty((need + 255,), dtype=torch.uint8, device=A.device)
+
+
 def forward_into(A: torch.Tensor, cfg: SolverConfig, evals: torch.Tensor,
                  evecs: torch.Tensor | None, status: torch.Tensor | None = None,
-                 steps: torch.Tensor | None = None, flags: torch.Tensor | None = None) -> None:
+                 steps: torch.Tensor | None = None, flags: torch.Tensor | None = None,
+                 ws: torch.Tensor | None = None) -> None:
     """Launch the forward on preallocated device tensors, stream-ordered,
-    without any host synchronisation (the C ABI call ``bed_forward_f32``)."""
+    without any host synchronisation (the C ABI call ``bed_forward_ws_f32``).
+    The n >= 9 workspace is ``ws`` (from :func:`workspace`) or, when omitted,
+    a fresh one from torch's caching allocator."""
     b, n, _ = A.shape
     ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    _native.forward_f32(A.data_ptr(), b, n, evals.data_ptr(),
-                        ptr(evecs) if cfg.compute_vectors else None,
-                        ptr(status), ptr(steps), ptr(flags),
-                        _native.make_config(cfg, n), _stream_handle(A.device))
+    if ws is None and n > 8:
+        ws = workspace(A, cfg)
+    wp, wb = 0, 0
+    if ws is not None:
+        wp = (ws.data_ptr() + 255) & ~255
+        wb = ws.numel() - (wp - ws.data_ptr())
+    _native.forward_ws_f32(A.data_ptr(), b, n, evals.data_ptr(),
+                           ptr(evecs) if cfg.compute_vectors else None,
+                           ptr(status), ptr(steps), ptr(flags),
+                           _native.make_config(cfg, n), wp or None, wb, _stream_handle(A.device))
 
 
 def _raise_for_status(A: torch.Tensor, status: torch.Tensor, flags: int, cfg: SolverConfig) -> None:
@@ -140,20 +163,36 @@ def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
 
 
 def taylor_backward(V: torch.Tensor, evals: torch.Tensor, g_v: torch.Tensor | None,
-                    g_evals: torch.Tensor | None, degree: int = TAYLOR_DEGREE) -> torch.Tensor:
+                    g_evals: torch.Tensor | None, degree: int = TAYLOR_DEGREE,
+                    check: bool = False) -> torch.Tensor:
     """gA = sym(V (F o (V^T gV) + diag(gL)) V^T) with the Taylor-K F (C ABI
-    ``bed_backward_f32``).  Missing cotangents are zero."""
+    ``bed_backward_f32``).  Missing cotangents are zero.
+
+    The series is the paper's for positive spectra.  A
+    pair outside its domain (larger eigenvalue <= 0, or a smaller one <= its
+    negative) takes the exact 1/(l_j - l_i); with ``check=True`` such a
+    matrix raises ``NonPositiveSpectrum`` (one host read of the flags word),
+    otherwise the exact fallback is used silently.
+    """
     V = _check_cuda_f32(V, "V")
     evals = _check_cuda_f32(evals, "evals")
     b, n, _ = V.shape
     gv = None if g_v is None else _check_cuda_f32(g_v, "g_v")
     gl = None if g_evals is None else _check_cuda_f32(g_evals, "g_evals")
     gA = torch.empty_like(V)
+    status = torch.empty((b,), device=V.device, dtype=torch.int32) if check else None
+    flags = torch.empty((1,), device=V.device, dtype=torch.int32) if check else None
     with torch.cuda.device(V.device):
         _native.backward_f32(V.data_ptr(), evals.data_ptr(),
                              None if gv is None else gv.data_ptr(),
                              None if gl is None else gl.data_ptr(),
-                             gA.data_ptr(), b, n, int(degree), _stream_handle(V.device))
+                             gA.data_ptr(), b, n, int(degree),
+                             None if status is None else status.data_ptr(),
+                             None if flags is None else flags.data_ptr(),
+                             _stream_handle(V.device))
+    if check and int(flags.item()) & (1 << _native.STATUS_NON_POSITIVE):
+        k = int(torch.nonzero(status == _native.STATUS_NON_POSITIVE)[0, 0])
+        raise NonPositiveSpectrum(k, float(evals[k].min()))
     return gA
 
 
@@ -161,8 +200,10 @@ class BatchedEigFn(torch.autograd.Function):
     """Differentiable batched ED: forward = ``bed_forward_f32``, backward =
     the Taylor-polynomial gradient ``bed_backward_f32`` (degree 9 by default).
 
-    ``check=False`` skips the host read of the status word, keeping the
-    forward free of device-to-host synchronisation (for training loops).
+    ``check=False`` skips the host reads of the status words, keeping the
+    forward and backward free of device-to-host synchronisation (for training
+    loops); with ``check=True`` the backward also raises NonPositiveSpectrum
+    for a spectrum outside the Taylor series' domain (see taylor_backward).
     """
 
     @staticmethod
@@ -174,12 +215,13 @@ class BatchedEigFn(torch.autograd.Function):
         evals, evecs, _, _ = _solve_device(A.detach(), cfg, check=check)
         ctx.save_for_backward(evals, evecs)
         ctx.degree = degree
+        ctx.check = check
         return evals, evecs
 
     @staticmethod
     def backward(ctx, g_evals, g_evecs):
         evals, evecs = ctx.saved_tensors
-        gA = taylor_backward(evecs, evals, g_evecs, g_evals, ctx.degree)
+        gA = taylor_backward(evecs, evals, g_evecs, g_evals, ctx.degree, ctx.check)
         return gA, None, None, None
 
 

@@ -90,3 +90,54 @@ def test_large_degree_approaches_exact_gradient(bed):
     sign = torch.sign((ve * r.eigenvectors.double()).sum(1, keepdim=True))
     ((ve * sign) * gv.double()).sum().backward()
     assert P.grad_err(g200.cpu().numpy(), ad.grad.cpu().numpy()).max() <= 1e-4
+
+
+@pytest.mark.parametrize("n,b,m", [(16, 65536, 64), (64, 8192, 256)])
+def test_backward_full_size_configs(bed, n, b, m):
+    """C4 (16 x 16, 65536) and C5 (64 x 64, 8192) at full size: the covariance
+    inputs of SURVEY 8(d); the oracle on a sample, symmetry on all."""
+    from paper_2207_04228_b200.datagen import covariance_device
+
+    a = covariance_device(b, n, m, n)
+    r = bed.batched_eig(a, bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n))
+    g = torch.Generator(device="cuda").manual_seed(17)
+    gv = torch.randn((b, n, n), device="cuda", generator=g)
+    gl = torch.randn((b, n), device="cuda", generator=g)
+    ga = bed.taylor_backward(r.eigenvectors, r.eigenvalues, gv, gl, check=True)
+    assert torch.equal(ga, ga.transpose(1, 2))
+    idx = torch.randperm(b, generator=torch.Generator().manual_seed(2))[:128].cuda()
+    ref = oracle.taylor_backward(r.eigenvectors[idx].cpu().numpy(), r.eigenvalues[idx].cpu().numpy(),
+                                 gv[idx].cpu().numpy(), gl[idx].cpu().numpy())
+    assert P.grad_err(ga[idx].cpu().numpy(), ref).max() <= P.GRAD_TOL
+
+
+def test_backward_outside_taylor_domain(bed):
+    """Indefinite / non-positive spectra: pairs outside the series' domain take
+    the exact 1/(l_j - l_i) and the matrix is flagged (NonPositiveSpectrum
+    with check=True); the oracle applies the same rule."""
+    n, b = 6, 40
+    rng = np.random.default_rng(9)
+    q, _ = np.linalg.qr(rng.standard_normal((b, n, n)))
+    lam = np.sort(rng.uniform(-3.0, 3.0, (b, n)), axis=1)[:, ::-1]
+    lam[:4] = np.abs(lam[:4]) + 0.5  # the first four are SPD
+    a = ((q * lam[:, None, :]) @ q.transpose(0, 2, 1)).astype(np.float32)
+    a = (a + a.transpose(0, 2, 1)) / 2
+    r = bed.batched_eig(torch.from_numpy(a).cuda(), bed.SolverConfig(deflation_tol=3e-12))
+    gv = torch.from_numpy(rng.standard_normal((b, n, n)).astype(np.float32)).cuda()
+    ga = bed.taylor_backward(r.eigenvectors, r.eigenvalues, gv, None)
+    ref = oracle.taylor_backward(r.eigenvectors.cpu().numpy(), r.eigenvalues.cpu().numpy(),
+                                 gv.cpu().numpy(), None)
+    assert P.grad_err(ga.cpu().numpy(), ref).max() <= P.GRAD_TOL
+    inside = oracle.taylor_domain(r.eigenvalues.cpu().numpy())
+    assert inside[:4].all() and not inside.all()
+    with pytest.raises(bed.NonPositiveSpectrum) as err:
+        bed.taylor_backward(r.eigenvectors, r.eigenvalues, gv, None, check=True)
+    assert err.value.batch_index == int(np.nonzero(~inside)[0][0])
+    # SPD only: no error with check
+    bed.taylor_backward(r.eigenvectors[:4].contiguous(), r.eigenvalues[:4].contiguous(), gv[:4].contiguous(),
+                        None, check=True)
+    # through autograd with check=True
+    at = torch.from_numpy(a).cuda().requires_grad_(True)
+    lam_t, v_t = bed.eigh(at, bed.SolverConfig(deflation_tol=3e-12), check=True)
+    with pytest.raises(bed.NonPositiveSpectrum):
+        (v_t * gv).sum().backward()

@@ -67,7 +67,7 @@ def test_known_answers(bed, known):
     np.testing.assert_allclose(vec, known["classic2x2/evecs"], rtol=2e-7)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 13, 16, 20, 24, 31, 32, 33, 40, 48, 57, 64])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 13, 16, 17, 20, 23, 24, 25, 31, 32, 33, 40, 48, 57, 64])
 def test_every_size_against_oracle(bed, n):
     b = 37 if n > 8 else 301  # ragged: not a multiple of any CTA tile
     a = oracle.gen_spd(b, n, 1000 + n).astype(np.float32)
@@ -211,3 +211,99 @@ def test_large_batch_properties(bed, n, b):
     idx = torch.randperm(b, generator=torch.Generator().manual_seed(0))[:64]
     o = oracle.forward(a[idx.cuda()].double().cpu().numpy())
     assert np.all(P.eig_err(lam[idx.cuda()].cpu().numpy(), o.eigenvalues) <= P.EIG_TOL)
+
+
+def test_values_only_matches_reference_fixture(bed, cells):
+    """The reference's own values-only output (solver.py:94-109, written by
+    tests/golden/make_golden.py with tol 3e-12, budget 32)."""
+    vals, vec, _ = _solve(bed, cells["n8_b64/a"], compute_vectors=False, **VERIFY)
+    assert vec is None
+    assert np.all(P.eig_err(vals, cells["n8_b64/values_only/evals"]) <= P.EIG_TOL)
+    full, _, _ = _solve(bed, cells["n8_b64/a"], **VERIFY)
+    assert np.all(P.eig_err(full, cells["n8_b64/values_only/evals"]) <= P.EIG_TOL)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 9, 12, 16, 17, 20, 24, 25, 31, 32, 33, 48, 64])
+@pytest.mark.parametrize("sort", ["descending", "ascending", "none"])
+def test_values_only_against_oracle(bed, n, sort):
+    b = 37 if n > 8 else 301
+    a = oracle.gen_spd(b, n, 2000 + n).astype(np.float32)
+    vals, vec, _ = _solve(bed, a, compute_vectors=False, sort=sort, **VERIFY)
+    o = oracle.forward(a.astype(np.float64), compute_vectors=False, sort=sort)
+    if sort == "none":  # unsorted order is the band order of each implementation
+        vals, ref = np.sort(vals, axis=1), np.sort(o.eigenvalues, axis=1)
+    else:
+        ref = o.eigenvalues
+    assert np.all(P.eig_err(vals, ref) <= P.EIG_TOL)
+
+
+@pytest.mark.parametrize("n,b", [(12, 3001), (16, 5000), (24, 3000), (32, 2000), (40, 700), (64, 300)])
+@pytest.mark.parametrize("vectors", [True, False])
+def test_chunked_workspace_is_bitwise_identical(bed, n, b, vectors):
+    """A workspace smaller than the batch needs (bed_forward_workspace_bytes)
+    solves it in chunks; results must not depend on the chunking."""
+    from paper_2207_04228_b200 import _native
+
+    a = torch.from_numpy(oracle.gen_spd(b, n, 31).astype(np.float32)).cuda()
+    cfg = bed.SolverConfig(max_double_steps=4 * n, compute_vectors=vectors, **VERIFY)
+    c = _native.make_config(cfg, n)
+    full = _native.workspace_bytes(b, n, c)
+    smallest = _native.workspace_bytes(32, n, c)
+    assert 0 < smallest < full
+
+    def run(ws):
+        lam = torch.empty((b, n), device="cuda")
+        vec = torch.empty((b, n, n), device="cuda") if vectors else None
+        st = torch.empty((b,), device="cuda", dtype=torch.int32)
+        k = torch.empty((b,), device="cuda", dtype=torch.int32)
+        bed.forward_into(a, cfg, lam, vec, st, k, ws=ws)
+        return [t.cpu() for t in (lam, vec, st, k) if t is not None]
+
+    ref = run(bed.workspace(a, cfg))
+    for cap in (full // 3, smallest, smallest + 1000):
+        got = run(bed.workspace(a, cfg, max_bytes=cap))
+        for x, y in zip(got, ref):
+            assert torch.equal(x, y)
+    # below the 32-matrix minimum the call is rejected, nothing launched
+    with pytest.raises(_native.NativeError):
+        tiny = torch.empty((smallest // 2,), dtype=torch.uint8, device="cuda")
+        lam = torch.empty((b, n), device="cuda")
+        vec = torch.empty((b, n, n), device="cuda")
+        bed.forward_into(a, cfg, lam, vec, ws=tiny)
+
+
+def test_workspace_sizes_are_batch_linear_without_records(bed):
+    from paper_2207_04228_b200 import _native
+
+    for n in (9, 16, 20, 24):
+        c = _native.make_config(bed.SolverConfig(max_double_steps=4 * n), n)
+        # P, band, status: 4 (n^2 + 2n + 1) bytes per matrix (+ 256-byte alignment)
+        assert _native.workspace_bytes(65536, n, c) <= 65536 * 4 * (n * n + 2 * n + 1) + 5 * 256
+    assert _native.workspace_bytes(1000, 8, _native.make_config(bed.SolverConfig(), 8)) == 0
+
+
+def test_headline_inputs_c2(bed):
+    """The bench's headline workload exactly: 4,194,304 gen_spd_device 4x4
+    matrices, verify profile.  Invariants on every matrix, the oracle on a
+    sample (the same call bench.py times)."""
+    from paper_2207_04228_b200.datagen import gen_spd_device
+
+    b, n = 1 << 22, 4
+    a = gen_spd_device(b, n, 0)
+    r = bed.batched_eig(a, bed.SolverConfig(deflation_tol=3e-12, max_double_steps=16))
+    lam, v = r.eigenvalues, r.eigenvectors
+    eye = torch.eye(n, device="cuda", dtype=torch.float64)
+    for lo in range(0, b, 1 << 20):
+        ad, vd, ld = a[lo:lo + (1 << 20)].double(), v[lo:lo + (1 << 20)].double(), lam[lo:lo + (1 << 20)].double()
+        rec = torch.linalg.matrix_norm(ad @ vd - vd * ld[:, None, :]) / torch.linalg.matrix_norm(ad)
+        orth = torch.linalg.matrix_norm(vd.transpose(1, 2) @ vd - eye) / n
+        assert float(rec.max()) <= P.RECON_TOL
+        assert float(orth.max()) <= P.ORTH_TOL
+    assert bool((lam[:, 1:] <= lam[:, :-1]).all())
+    lead = torch.gather(v, 1, v.abs().argmax(dim=1, keepdim=True))
+    assert float(lead.min()) >= 0.0
+    assert int(r.diagnostics.converged_steps.max()) <= 16
+    idx = torch.randperm(b, generator=torch.Generator().manual_seed(1))[:256].cuda()
+    o = oracle.forward(a[idx].double().cpu().numpy())
+    assert np.all(P.eig_err(lam[idx].cpu().numpy(), o.eigenvalues) <= P.EIG_TOL)
+    assert np.all(P.vector_err(v[idx].cpu().numpy(), o.eigenvectors, o.eigenvalues) <= 1.0)

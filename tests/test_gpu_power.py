@@ -151,3 +151,30 @@ def test_scatter_matches_float64(bed, n, m, eps):
     err = np.linalg.norm(out - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
     assert err.max() <= 1e-5, err.max()
     np.testing.assert_array_equal(out, out.transpose(0, 2, 1))
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 8, 12, 16, 32, 64])
+def test_scatter_full_ctas(bed, n):
+    """Batches that fill every matrix slot of the producer's CTAs (128 / (n/4)^2
+    matrices per CTA for n <= 32) -- each (matrix, channel) row sum has an owner."""
+    m = 2 * n + 3
+    b = 1024 if n <= 32 else 300
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal((b, n, m)) * 2.0 + rng.standard_normal((b, n, 1)) * 5.0).astype(np.float32)
+    out = bed.scatter_matrices(torch.from_numpy(x).cuda(), 1e-3).cpu().numpy().astype(np.float64)
+    xc = x.astype(np.float64) - x.astype(np.float64).mean(axis=2, keepdims=True)
+    ref = xc @ xc.transpose(0, 2, 1)
+    ref = (ref + ref.transpose(0, 2, 1)) / 2 + 1e-3 * np.eye(n)
+    err = np.linalg.norm(out - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
+    assert err.max() <= 1e-5, (err.max(), int(err.argmax()))
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_zca_large_batch(bed, n):
+    b, m = 2048, 8 * n
+    x = torch.randn(b, n, m, device="cuda", generator=torch.Generator(device="cuda").manual_seed(n))
+    out = bed.zca_whiten(x, 1e-4).data
+    c = out.double() - out.double().mean(dim=2, keepdim=True)
+    cov = c @ c.transpose(1, 2)
+    # eps_reg shrinks the whitened scatter slightly below I
+    assert float((cov - torch.eye(n, device="cuda", dtype=torch.float64)).abs().max()) <= 2e-2

@@ -21,12 +21,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_library_exports_every_header_symbol():
     header = open(os.path.join(ROOT, "include", "bed200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(bed_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(bed_\w+)\s*\(", header, re.M))
     assert declared == set(_native.EXPORTS)
     L = _native.lib()
     for sym in declared:
         assert getattr(L, sym) is not None
-    assert L.bed_abi_version() == 1
+    assert L.bed_abi_version() == 2
     assert b"invalid" in L.bed_error_string(1)
 
 
@@ -38,7 +38,16 @@ def test_abi_argument_checks_need_no_gpu():
     # n out of range / null output: rejected before any CUDA call
     assert L.bed_forward_f32(None, 1, 0, None, None, None, None, None, ctypes.byref(cfg), None) == 1
     assert L.bed_forward_f32(None, 1, 65, None, None, None, None, None, ctypes.byref(cfg), None) == 1
-    assert L.bed_backward_f32(None, None, None, None, None, 1, 4, -1, None) == 1
+    assert L.bed_backward_f32(None, None, None, None, None, 1, 4, -1, None, None, None) == 1
+    # workspace queries are host arithmetic: exact without a GPU
+    c16 = _native.make_config(bed.SolverConfig(max_double_steps=64), 16)
+    assert _native.workspace_bytes(0, 16, c16) == 0
+    assert _native.workspace_bytes(1000, 4, c16) == 0
+    w32 = _native.workspace_bytes(32, 16, c16)
+    assert 0 < w32 < _native.workspace_bytes(64, 16, c16) < _native.workspace_bytes(1 << 20, 16, c16)
+    # below the 32-matrix minimum: rejected before any CUDA call
+    assert L.bed_forward_ws_f32(1 << 20, 100, 16, 1 << 20, 1 << 20, None, None, None, ctypes.byref(c16),
+                                1 << 20, w32 - 1, None) == 1
     bad = _native.BedConfig(1e-5, 1e-12, 8, 7, 1, 0)  # bad sort code
     assert L.bed_forward_f32(None, 0, 4, None, None, None, None, None, ctypes.byref(bad), None) == 1
 

@@ -8,7 +8,7 @@ import paper_2207_04228_b200 as bed  # noqa: E402
 from paper_2207_04228_b200.datagen import covariance_device, gen_spd_device  # noqa: E402
 
 torch.cuda.set_device(0)
-cases = [(4, 1 << 22, False), (8, 1 << 20, False), (16, 65536, True), (32, 65536, False),
+cases = [(4, 1 << 22, False), (8, 1 << 20, False), (16, 65536, True), (24, 65536, False), (32, 65536, False),
          (64, 8192, True)]
 which = [x for x in sys.argv[1:] if x.isdigit()] or None
 power = "pow" in sys.argv
