@@ -108,9 +108,11 @@ int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, floa
  * matrices of order n in one pass; 0 for n <= 8 (or batch <= 0).  The
  * smallest workspace accepted is bed_forward_workspace_bytes(32, n, cfg):
  * between the two, the batch is solved in chunks of whole multiples of 32.
- * For 9 <= n <= 24 (and for values-only solves) it is 4 (n^2 + 2n + 1) bytes
- * per matrix with vectors; for 25 <= n <= 64 with vectors it adds the
- * rotation record of every sweep the double-step budget allows. */
+ * Values-only: 4 (2n + 1) bytes per matrix (the band, a status).  With
+ * vectors: plus P (4 n^2 bytes), the unsorted eigenvalues (4 n) and the
+ * rotation record the band QR streams to the eigenvector fold -- every sweep
+ * the double-step budget allows (2 max_double_steps + 1), NMAX - 1 positions
+ * of 8 bytes (NMAX = 16, 24, 32 or 64, the size tier of n). */
 size_t bed_forward_workspace_bytes(int64_t batch, int32_t n, const bed_config* cfg);
 
 /* bed_forward_f32 with a caller-owned device workspace (256-byte aligned,

@@ -1,0 +1,309 @@
+// bed_fold_tma.cuh -- F stage of the split medium path: fold the rotation
+// record of bed_qr_kernel into V = P (the column updates of _kernels.py:
+// 269-277; V starts as P = H_0 H_1 ..., so V = P Q of solver.py:93 needs no
+// GEMM), then stable sort + sign (solver.py:60-76) and coalesced stores.
+//
+// A CTA owns MPC consecutive matrices of one band warp.  A producer warp
+// streams that warp's sweep records global -> shared with bulk async copies
+// (TMA engine, cp.async.bulk: one copy per sweep of the rows its extent
+// covers, all 32 lanes -- the CTAs sharing a band warp read it from L2) into
+// an NB-deep ring; each slot completes an mbarrier by transaction count.  The fold
+// threads -- LF per matrix, R rows of V each, held in registers (packed row
+// pairs for R even, so a rotation of two columns costs 2 FMUL2 + 2 FFMA2 per
+// two rows) -- wait on the slot's barrier, apply the sweep, and release the
+// slot through a second mbarrier.  Each fold warp applies only the
+// positions its own matrices need (the largest active size among them, put
+// in the slot header by the producer; the record holds exact identities past
+// a matrix's block), in blocks of BLK positions whose rotations are loaded
+// ahead of the arithmetic, and skips sweeps in which all of them sit out.
+#pragma once
+
+#include "bed_f32x2.cuh"
+#include "bed_split_ws.cuh"
+#include "bed_tile.cuh"
+
+namespace bed {
+
+template <int NMAX>
+struct FTParams {
+  static constexpr int LF = NMAX <= 16 ? 4 : (NMAX <= 24 ? 6 : (NMAX <= 32 ? 16 : 32));
+  static constexpr int R = NMAX / LF;     // rows per fold thread: 4, 4, 2, 2
+  static constexpr int RP = (R + 1) / 2;  // packed row pairs (R = 1: scalar rows)
+  static constexpr int MPC = NMAX <= 16 ? 32 : (NMAX <= 32 ? 16 : 8);
+  static constexpr int FT = MPC * LF;
+  static constexpr int THREADS = FT + 32;  // + the producer warp
+  static constexpr int MINB = NMAX <= 24 ? 4 : (NMAX <= 32 ? 2 : 1);
+  static constexpr int NB = 6;
+  static constexpr int NW = FT / 32;   // fold warps
+  static constexpr int BLK = kFoldBlk;  // positions per fold block (one branch, loads hoisted)
+  static constexpr int POS = NMAX - 1;
+  static constexpr int SLOT = POS * 32;  // float2 per ring slot: a whole sweep record [position][lane]
+  static constexpr int RING = NB * SLOT * 2;
+  static constexpr int SROW = NMAX + 1;
+  static constexpr int SMAT = NMAX * SROW;
+  static constexpr int STAGE = MPC * SMAT;
+  static constexpr int U = ((RING > STAGE ? RING : STAGE) + 3) / 4 * 4;
+  static constexpr int OFF_LAM = U;
+  static constexpr int OFF_EV = OFF_LAM + MPC * NMAX;
+  static constexpr int OFF_RANK = OFF_EV + MPC * NMAX;
+  static constexpr int OFF_FLIP = OFF_RANK + MPC * NMAX;
+  static constexpr int OFF_BAR = (OFF_FLIP + MPC * NMAX + 1) / 2 * 2;  // 8-byte aligned
+  static constexpr int OFF_HDR = OFF_BAR + 2 * 2 * NB;                 // full[NB], empty[NB]
+  static constexpr int TOTAL = OFF_HDR + NB * NW;                      // per slot: each fold warp's extent
+  static constexpr size_t BYTES = sizeof(float) * (size_t)TOTAL;
+  static_assert(R * LF == NMAX && (R % 2 == 0 || R == 1), "row split");
+  static_assert(FT % 32 == 0 && 32 % MPC == 0, "CTA = whole warps, one band warp's lanes");
+  static_assert((MPC * 8) % 16 == 0, "bulk copies move multiples of 16 bytes");
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy on the TMA engine, completing `bytes` on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NMAX, bool EXACT>
+__global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
+    bed_fold_tma_kernel(int64_t bc, int64_t c0, int n_rt, SplitWs ws, float* __restrict__ evals,
+                        float* __restrict__ evecs, KernelCfg cfg) {
+  using P = FTParams<NMAX>;
+  constexpr int LF = P::LF, R = P::R, RP = P::RP, MPC = P::MPC, NB = P::NB, POS = P::POS;
+  const int n = EXACT ? NMAX : n_rt;
+  const int nn = n * n;
+  extern __shared__ __align__(16) float smem[];
+  float2* ring = reinterpret_cast<float2*>(smem);
+  float* lams = smem + P::OFF_LAM;
+  float* evs = smem + P::OFF_EV;
+  int* ranks = reinterpret_cast<int*>(smem + P::OFF_RANK);
+  float* flipv = smem + P::OFF_FLIP;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P::OFF_BAR);
+  uint64_t* empty = full + NB;
+  const int tid = threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.x * MPC;
+  const int count = (bc - j0) < MPC ? (int)(bc - j0) : MPC;
+  const int64_t w = j0 >> 5;            // band warp of the chunk
+  const int lane0 = (int)(j0 & 31);     // its first lane in this CTA
+  const int nrec = ws.nsw[w];
+  const int* msw = ws.msw + (size_t)w * ws.Smax;
+  const uint8_t* mls = ws.mlane + (size_t)w * ws.Smax * 32 + lane0;
+  const float2* recw = ws.rot + (size_t)w * ws.Smax * POS * 32;  // the band warp's record
+
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(empty + b, P::FT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int mi = tid / LF, l = tid % LF;
+  const bool mlive = tid < P::FT && mi < count;
+  if (mlive) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int c = l + LF * rr;
+      if (c < n) lams[mi * NMAX + c] = ws.lam[(int64_t)c * ws.Bc + j0 + mi];
+    }
+  }
+  __syncthreads();
+
+  // V rows: packed pairs (rows l + LF * 2rp, l + LF * (2rp + 1)) or, for
+  // R = 1, one scalar row l
+  f2 v[RP][NMAX];
+  float vs[R == 1 ? NMAX : 1];
+
+  if (tid >= P::FT) {
+    // ------------------------------------------------------------ producer warp
+    // Per sweep: the warp's extent (msw) bounds the rows to copy -- Q wrote
+    // every row up to the fold-block boundary past it (identities beyond a
+    // lane's block) -- and each fold warp's extent (the largest active size
+    // among its matrices, from mlane) goes into the slot header.
+    const int lane = tid & 31;
+    int* hdr = reinterpret_cast<int*>(smem + P::OFF_HDR);
+#pragma unroll 1
+    for (int s0 = 0; s0 < nrec; s0 += 32) {
+      const int mw_l = s0 + lane < nrec ? __ldg(msw + s0 + lane) : 0;  // 32 sweeps per load
+      int ml_next = lane < MPC ? mls[(size_t)s0 * 32 + lane] : 0;
+#pragma unroll 1
+      for (int s = s0; s < min(nrec, s0 + 32); ++s) {
+        const int b = s % NB;
+        const int ml = ml_next;
+        if (s + 1 < nrec && lane < MPC) ml_next = mls[(size_t)(s + 1) * 32 + lane];
+        const int mw = __shfl_sync(0xffffffffu, mw_l, s - s0);
+        const int np = min(POS, (mw - 1 + kFoldBlk - 1) / kFoldBlk * kFoldBlk);
+        if (s >= NB) mbar_wait(empty + b, ((s / NB) & 1) ^ 1);
+#pragma unroll
+        for (int f = 0; f < P::NW; ++f) {
+          const int lo = (32 * f) / LF, hi = (32 * f + 31) / LF;
+          const int wmf = __reduce_max_sync(0xffffffffu, (lane >= lo && lane <= hi) ? ml : 0);
+          if (lane == 0) hdr[b * P::NW + f] = wmf;
+        }
+        __syncwarp();
+        if (lane == 0) {  // rows 0 .. np-1 of the sweep record: one contiguous bulk copy
+          mbar_arrive_tx(full + b, (unsigned)(np * 32 * 8));
+          bulk_g2s(ring + b * P::SLOT, recw + (size_t)s * POS * 32, np * 32 * 8, full + b);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ fold threads
+    const float* pm = ws.P + (j0 + mi) * nn;
+    if constexpr (R == 1) {
+      const bool ok = mlive && l < n;
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c) vs[c] = (ok && c < n) ? __ldg(pm + l * n + c) : 0.0f;
+    } else {
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+        const int r0 = l + LF * (2 * rp), r1 = r0 + LF;
+        const bool ok0 = mlive && r0 < n, ok1 = mlive && r1 < n;
+        if (EXACT && NMAX % 4 == 0) {
+#pragma unroll
+          for (int c4 = 0; c4 < NMAX / 4; ++c4) {
+            const float4 x = ok0 ? __ldg(reinterpret_cast<const float4*>(pm + r0 * NMAX) + c4)
+                                 : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            const float4 y = ok1 ? __ldg(reinterpret_cast<const float4*>(pm + r1 * NMAX) + c4)
+                                 : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            v[rp][4 * c4] = f2_make(x.x, y.x);
+            v[rp][4 * c4 + 1] = f2_make(x.y, y.y);
+            v[rp][4 * c4 + 2] = f2_make(x.z, y.z);
+            v[rp][4 * c4 + 3] = f2_make(x.w, y.w);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NMAX; ++c) {
+            const float x = (ok0 && c < n) ? __ldg(pm + r0 * n + c) : 0.0f;
+            const float y = (ok1 && c < n) ? __ldg(pm + r1 * n + c) : 0.0f;
+            v[rp][c] = f2_make(x, y);
+          }
+        }
+      }
+    }
+    const int* hdr = reinterpret_cast<const int*>(smem + P::OFF_HDR) + (tid >> 5);
+#pragma unroll 1
+    for (int s = 0; s < nrec; ++s) {
+      const int b = s % NB;
+      mbar_wait(full + b, (s / NB) & 1);
+      const int wm = hdr[b * P::NW];  // positions 0 .. wm - 2 hold this warp's rotations
+      const float2* rs = ring + b * P::SLOT + lane0 + mi;
+      static_for<0, (POS + P::BLK - 1) / P::BLK>([&](auto bcst) {
+        constexpr int p0 = decltype(bcst)::value * P::BLK;
+        constexpr int p1 = p0 + P::BLK < POS ? p0 + P::BLK : POS;
+        if (p0 < wm - 1) {  // the block's rows were copied (whole fold blocks)
+          float2 cs[P::BLK];
+#pragma unroll
+          for (int p = p0; p < p1; ++p) cs[p - p0] = rs[p * 32];
+#pragma unroll
+          for (int p = p0; p < p1; ++p) {
+            if constexpr (R == 1) {
+              const float x = vs[p], y = vs[p + 1];
+              vs[p] = cs[p - p0].x * x - cs[p - p0].y * y;
+              vs[p + 1] = fmaf(cs[p - p0].y, x, cs[p - p0].x * y);
+            } else {
+#pragma unroll
+              for (int rp = 0; rp < RP; ++rp)
+                rot2(v[rp][p], v[rp][p + 1], cs[p - p0].x, cs[p - p0].y, -cs[p - p0].y);
+            }
+          }
+        }
+      });
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(empty + b);
+    }
+  }
+  __syncthreads();  // every slot was consumed: the ring is free for the stage
+
+  // ---- stable sort + sign (solver.py:60-76): fold thread l ranks columns l + LF * rr
+  float* st = smem + (tid < P::FT ? mi : 0) * P::SMAT;
+  if (mlive) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int c = l + LF * rr;
+      if (c < n) {
+        const float lc = lams[mi * NMAX + c];
+        int rk = c;
+        if (cfg.sort != 0) {
+          rk = 0;
+          for (int k = 0; k < n; ++k)
+            rk += (k != c && rank_before(lams[mi * NMAX + k], k, lc, c, cfg.sort)) ? 1 : 0;
+        }
+        ranks[mi * NMAX + c] = rk;
+        evs[mi * NMAX + rk] = lc;
+      }
+    }
+  }
+  __syncthreads();
+  if (mlive) {
+    if constexpr (R == 1) {
+#pragma unroll
+      for (int c = 0; c < NMAX; ++c)
+        if (c < n && l < n) st[l * P::SROW + ranks[mi * NMAX + c]] = vs[c];
+    } else {
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+        const int r0 = l + LF * (2 * rp), r1 = r0 + LF;
+#pragma unroll
+        for (int c = 0; c < NMAX; ++c) {
+          if (c < n) {
+            const int rk = ranks[mi * NMAX + c];
+            if (r0 < n) st[r0 * P::SROW + rk] = f2_lo(v[rp][c]);
+            if (r1 < n) st[r1 * P::SROW + rk] = f2_hi(v[rp][c]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (mlive) {  // sign: the largest-magnitude entry of each column is >= 0
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int c = l + LF * rr;
+      if (c < n) {
+        float best = -1.0f, lead = 0.0f;
+        for (int r = 0; r < n; ++r) {
+          const float x = st[r * P::SROW + c];
+          if (fabsf(x) > best) {
+            best = fabsf(x);
+            lead = x;
+          }
+        }
+        flipv[mi * NMAX + c] = lead < 0.0f ? -1.0f : 1.0f;
+      }
+    }
+  }
+  __syncthreads();
+  stage_to_tile<NMAX, P::THREADS, P::SROW, P::SMAT>(smem, count, n, evecs + (c0 + j0) * nn, flipv);
+  float* dstl = evals + (c0 + j0) * n;
+  for (int g = tid; g < count * n; g += P::THREADS) {
+    const int mat = g / n, c = g - mat * n;
+    dstl[g] = evs[mat * NMAX + c];
+  }
+}
+
+}  // namespace bed

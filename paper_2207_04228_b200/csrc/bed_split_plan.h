@@ -14,17 +14,10 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Tier order (NMAX) of the medium path for n in [9, 64].
 inline int split_nmax(int n) { return n <= 16 ? 16 : (n <= 24 ? 24 : (n <= 32 ? 32 : 64)); }
-// n <= 24 with vectors: the fused band-QR + fold kernel (bed_qf.cuh) takes
-// the rotations through shared memory, so no rotation record exists.  From
-// n = 32 on, a CTA's V's fill the register file with too few band chains in
-// flight per SM to hide the sweep latency (measured at n = 32, 65536
-// matrices: 1.85 ms fused vs 1.40 ms split), so n > 24 keeps the Q/F pair.
-inline bool split_fused(int nmax) { return nmax <= 24; }
-
 // Workspace of one chunk of Bc matrices (Bc a multiple of 32), carved from one
 // caller-provided block: P (the initial V), the band, the validation status
-// and -- for the unfused tiers -- the rotation record of the Q/F pair, which
-// holds every sweep the double-step budget allows (2 * max_steps + 1).
+// and, with vectors, the rotation record Q writes and F reads, which holds
+// every sweep the double-step budget allows (2 * max_steps + 1).
 struct SplitPlan {
   int64_t Bc = 0;
   size_t bytes = 0, oP = 0, oD = 0, oE = 0, oL = 0, oV = 0, oR = 0, oM = 0, oN = 0, oML = 0;
@@ -32,7 +25,7 @@ struct SplitPlan {
 
 inline SplitPlan split_plan(int64_t Bc, int n, bool vecs, int max_steps) {
   const int nmax = split_nmax(n);
-  const bool rec = vecs && !split_fused(nmax);
+  const bool rec = vecs;
   const size_t smax = 2 * (size_t)max_steps + 1;
   const size_t W = (size_t)Bc / 32, nn = (size_t)n * n;
   SplitPlan p;

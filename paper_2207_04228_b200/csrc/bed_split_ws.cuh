@@ -6,7 +6,9 @@
 
 namespace bed {
 
-constexpr int kFoldBlk = 8;    // positions per static fold block
+// positions per record block: Q pads each sweep's record with identities to
+// a whole block, F copies and applies whole blocks
+constexpr int kFoldBlk = 4;
 constexpr int kQThreads = 32;  // one warp per CTA: small batches (n = 64) still reach every SM
 
 struct SplitWs {

@@ -272,13 +272,21 @@ def test_chunked_workspace_is_bitwise_identical(bed, n, b, vectors):
         bed.forward_into(a, cfg, lam, vec, ws=tiny)
 
 
-def test_workspace_sizes_are_batch_linear_without_records(bed):
+def test_workspace_sizes(bed):
+    """Values-only: the band and status, 4 (2n + 1) bytes per matrix.  With
+    vectors: plus P (4 n^2) and the rotation record of every sweep the budget
+    allows (2 * budget + 1 sweeps of the tier's NMAX - 1 positions, 8 bytes
+    each, plus a 4-byte extent per warp-sweep and a 1-byte size per lane)."""
     from paper_2207_04228_b200 import _native
 
-    for n in (9, 16, 20, 24):
+    b = 65536
+    for n, nmax in ((9, 16), (16, 16), (20, 24), (24, 24), (32, 32), (40, 64), (64, 64)):
+        cv = _native.make_config(bed.SolverConfig(max_double_steps=4 * n, compute_vectors=False), n)
+        assert b * 4 * (2 * n + 1) <= _native.workspace_bytes(b, n, cv) <= b * 4 * (2 * n + 1) + 4 * 256
         c = _native.make_config(bed.SolverConfig(max_double_steps=4 * n), n)
-        # P, band, status: 4 (n^2 + 2n + 1) bytes per matrix (+ 256-byte alignment)
-        assert _native.workspace_bytes(65536, n, c) <= 65536 * 4 * (n * n + 2 * n + 1) + 5 * 256
+        smax = 8 * n + 1
+        want = b * (4 * (n * n + 3 * n + 1) + smax * (nmax - 1) * 8 + smax) + (b // 32) * (4 * smax + 4)
+        assert want <= _native.workspace_bytes(b, n, c) <= want + 9 * 256
     assert _native.workspace_bytes(1000, 8, _native.make_config(bed.SolverConfig(), 8)) == 0
 
 

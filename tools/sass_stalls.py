@@ -35,3 +35,25 @@ print("samples per 1 KB of code:")
 for k in sorted(reg):
     if reg[k] > 0.01 * tot:
         print(f"  +0x{k*1024:05x}: {100*reg[k]/tot:5.1f}%")
+
+# stall reasons summed over an address range: [lo-hi] as hex offsets
+if len(sys.argv) > 3:
+    lo, hi = (int(x, 16) for x in sys.argv[3].split("-"))
+    cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    sums = {hdr[i]: 0.0 for i in cols}
+    n_ex = 0
+    for r in data:
+        off = int(r[ia], 16) - base
+        if lo <= off < hi:
+            for i in cols:
+                try:
+                    sums[hdr[i]] += float(r[i])
+                except ValueError:
+                    pass
+            try:
+                n_ex += int(r[iexe])
+            except ValueError:
+                pass
+    print(f"range +0x{lo:x}-+0x{hi:x}: warp-instructions executed {n_ex}")
+    for k, v in sorted(sums.items(), key=lambda kv: -kv[1])[:10]:
+        print(f"  {k:28s} {v:8.0f}")
