@@ -243,6 +243,29 @@ def e2e_host(torch, bed, n, batch, steps, dev_index):
                     f"{steps} calls (chunked 3-stream copy/compute overlap)"}
 
 
+def e2e_numpy_api(bed, n, batch, steps):
+    """The reference-facing Python call exactly as a reference user makes it:
+    batched_eig(BatchedSymmetric(float64 numpy)) -> float64 numpy results
+    (solver.py:79-112): host float64 validation + symmetrisation, FP32 cast
+    into page-locked memory, H2D, solve, D2H, float64 results -- all timed."""
+    import oracle
+
+    a = oracle.gen_spd(min(batch, 1 << 20), n, 7)
+    cfg = bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n)
+    bed.batched_eig(bed.BatchedSymmetric(a), cfg)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        bed.batched_eig(bed.BatchedSymmetric(a), cfg)
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    b = a.shape[0]
+    return {"value": b / sec, "unit": UNIT, "batch": b, "h2d_bytes_per_step": 4 * b * n * n,
+            "d2h_bytes_per_step": 4 * b * (n * n + n) + 16 * b,
+            "path": "batched_eig(BatchedSymmetric(float64 numpy)), median of "
+                    f"{steps} calls (host float64 validate + cast dominate)"}
+
+
 def load_traffic(name):
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
@@ -307,6 +330,7 @@ def run_ours(args):
         dist.barrier()
     if rank == 0:
         line["e2e"] = e2e_host(torch, bed, n, batch, max(3, min(args.steps, 10)), local)
+        line["e2e_numpy_api"] = e2e_numpy_api(bed, n, batch, 3)
         if not args.quick:
             line["other_configs"] = other_configs(torch, bed, dev, hbm_peak)
         threads = os.cpu_count() or 1
@@ -324,27 +348,45 @@ def run_ours(args):
                                 "sample": f"{reps} x {sample} 4x4 matrices (same distribution), oracle/ "
                                           "C restatement of the reference solver, per-matrix gate, "
                                           f"tol {TOL:g}, budget 16, {threads} threads, {secs:.1f} s"}
-        try:
-            sub = step.a[:16384].contiguous()
-            torch.linalg.eigh(sub)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            torch.linalg.eigh(sub)
-            torch.cuda.synchronize()
-            te = time.perf_counter() - t0
-            line["torch_eigh_baseline"] = {"value": sub.shape[0] / te, "unit": UNIT,
-                                           "batch": sub.shape[0], "what": "torch.linalg.eigh fp32 on 1 B200"}
-        except Exception as exc:  # noqa: BLE001
-            line["torch_eigh_baseline"] = {"unavailable": str(exc)[:120]}
+        te = torch_eigh_ms(torch, step.a)
+        line["torch_eigh_baseline"] = (
+            {"value": batch / (te * 1e-3), "unit": UNIT, "batch": batch, "ms": te,
+             "what": "torch.linalg.eigh fp32 on the same resident batch, 1 B200, CUDA events"}
+            if te else {"unavailable": "torch.linalg.eigh failed"})
+        if not args.quick:
+            try:
+                line["reference_numba"] = reference_numba(n)
+            except Exception as exc:  # noqa: BLE001
+                line["reference_numba"] = {"unavailable": str(exc)[:160]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
+def torch_eigh_ms(torch, a, reps=3):
+    """torch.linalg.eigh (cuSOLVER batched syevj, FP32) on the same resident
+    batch: CUDA-event time per call, best of `reps` after one warm call."""
+    try:
+        torch.linalg.eigh(a)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.linalg.eigh(a)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return best
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def other_configs(torch, bed, dev, hbm_peak):
     """C1/C3 (b=512, launch-bound), C4 (n=16 fwd+bwd), C5 (n=64 fwd+bwd),
-    and the n sweep at large batch -- reported beside the headline."""
+    and the n sweep at large batch -- reported beside the headline, each with
+    torch.linalg.eigh on the same tensors (forward rows)."""
     rows = []
     cases = [(4, 512, "fwd"), (8, 512, "fwd"), (16, 512, "fwd"), (24, 512, "fwd"), (32, 512, "fwd"),
              (8, 1 << 20, "fwd"), (16, 1 << 18, "fwd"), (24, 1 << 17, "fwd"), (32, 1 << 16, "fwd"),
@@ -357,10 +399,81 @@ def other_configs(torch, bed, dev, hbm_peak):
         # size can pay one-off costs (module load, workspace pool growth)
         sec = min(time_steps(torch, st, reps, 5) for _ in range(3)) / reps
         bound, frac, _, _ = roofline(n, mode, b, sec, hbm_peak)
-        rows.append({"n": n, "batch": b, "mode": mode, "ms": sec * 1e3, "value": b / sec,
-                     "roofline_bound": bound, "roofline_frac": frac,
-                     "mean_double_steps": float(st.steps.float().mean())})
+        row = {"n": n, "batch": b, "mode": mode, "ms": sec * 1e3, "value": b / sec,
+               "roofline_bound": bound, "roofline_frac": frac,
+               "mean_double_steps": float(st.steps.float().mean())}
+        if mode == "fwd":
+            te = torch_eigh_ms(torch, st.a)
+            row["torch_eigh_ms"] = te
+            row["speedup_vs_torch_eigh"] = (te / (sec * 1e3)) if te else None
+        rows.append(row)
+        del st
+        torch.cuda.empty_cache()
     return rows
+
+
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+_NUMBA_CHUNK = {}
+
+
+def _numba_chunk(key):
+    """One chunk through the unmodified reference (baseline/_ref) in a forked
+    pool worker; the chunk itself was inherited through fork (no pickling)."""
+    import batchedeig as ref
+
+    a, n = _NUMBA_CHUNK[key]
+    cfg = ref.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n)
+    ref.batched_eig(ref.BatchedSymmetric(a), cfg)
+    return a.shape[0]
+
+
+def reference_numba(n, target_s=6.0):
+    """The UNMODIFIED reference package (pip-installed into baseline/_ref)
+    through its own public API: batchedeig.batched_eig on host arrays from
+    its own gen_spd, verify profile (bench.py:40, :227-228).  (i) as shipped,
+    one process on one batch; (ii) sharded over every host core (fork pool,
+    chunks of 4096 / 2048 / 256 matrices for n = 4 / 16 / 64).
+    None if baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(REF_PATH, "batchedeig")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import multiprocessing as mproc
+
+    import batchedeig as ref
+    from batchedeig.bench import gen_spd
+
+    cfg = ref.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n)
+    warm = gen_spd(64, n, 1, 3.0).data
+    ref.batched_eig(ref.BatchedSymmetric(warm), cfg)  # numba JIT / cache load
+    chunk = 4096 if n <= 4 else (2048 if n <= 16 else 256)
+    a = gen_spd(chunk, n, 2, 3.0).data
+    t0 = time.perf_counter()
+    ref.batched_eig(ref.BatchedSymmetric(a), cfg)
+    one = time.perf_counter() - t0
+    reps = max(1, int(target_s / 2 / max(one, 1e-6)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ref.batched_eig(ref.BatchedSymmetric(a), cfg)
+    single = chunk * reps / (time.perf_counter() - t0)
+    procs = os.cpu_count() or 1
+    jobs = ["run"] * max(procs, int(procs * single * target_s / 2 / chunk))
+    _NUMBA_CHUNK["warm"] = (warm, n)
+    _NUMBA_CHUNK["run"] = (a, n)
+    ctx = mproc.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_numba_chunk, ["warm"] * procs)  # JIT / cache load in every worker
+        t0 = time.perf_counter()
+        done = sum(pool.map(_numba_chunk, jobs))
+        multi = done / (time.perf_counter() - t0)
+    return {"as_shipped": {"value": single, "unit": UNIT, "cores": 1,
+                           "sample": f"{reps} x batched_eig on {chunk} {n}x{n} gen_spd matrices"},
+            "all_cores": {"value": multi, "unit": UNIT, "cores": procs,
+                          "sample": f"{len(jobs)} chunks of {chunk} over a {procs}-process fork pool"},
+            "kind": "reference", "path": "baseline/_ref batchedeig.batched_eig (numba "
+                                         "kernels, batch-wide deflation gate), verify profile"}
 
 
 def run_reference(args):
@@ -392,6 +505,10 @@ def run_reference(args):
                                    f"restatement of batchedeig.batched_eig), {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["reference_numba"] = reference_numba(n, target_s=4.0)
+    except Exception as exc:  # noqa: BLE001
+        line["reference_numba"] = {"unavailable": str(exc)[:160]}
     print(json.dumps(line), flush=True)
 
 

@@ -116,11 +116,19 @@ int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, floa
 size_t bed_forward_workspace_bytes(int64_t batch, int32_t n, const bed_config* cfg);
 
 /* bed_forward_f32 with a caller-owned device workspace (256-byte aligned,
- * ignored for n <= 8).  No allocation inside.  BED_ERR_INVALID_ARGUMENT if
- * it is smaller than bed_forward_workspace_bytes(32, n, cfg). */
+ * ignored for n <= 8) and the optional per-matrix diagnostics of the
+ * reference's SolveDiagnostics / NoConvergence (qr.py:101-118, :385-389):
+ *   diag   (batch, 3) int32  nullable; [rotations applied (sum of active - 1
+ *                            over the matrix's sweeps), reduction events
+ *                            (trailing deflations), step_r_sum (reductions
+ *                            so far, summed over its double steps)]
+ *   resid  (batch) float     nullable; largest active coupling (equilibrated
+ *                            band) left when the budget ran out, else 0
+ * No allocation inside.  BED_ERR_INVALID_ARGUMENT if the workspace is
+ * smaller than bed_forward_workspace_bytes(32, n, cfg). */
 int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
-                       int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
-                       void* workspace, size_t workspace_bytes, void* stream);
+                       int32_t* status, int32_t* steps, int32_t* flags, int32_t* diag, float* resid,
+                       const bed_config* cfg, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Same computation on HOST buffers (pinned or pageable), on CUDA device
  * `device`.  Streams the batch through the GPU in chunks with copies

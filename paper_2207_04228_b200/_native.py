@@ -71,8 +71,8 @@ def lib() -> ctypes.CDLL:
     L.bed_forward_f32.restype = ctypes.c_int
     L.bed_forward_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, ctypes.POINTER(BedConfig), vp]
     L.bed_forward_ws_f32.restype = ctypes.c_int
-    L.bed_forward_ws_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, ctypes.POINTER(BedConfig),
-                                     vp, ctypes.c_size_t, vp]
+    L.bed_forward_ws_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp,
+                                     ctypes.POINTER(BedConfig), vp, ctypes.c_size_t, vp]
     L.bed_forward_workspace_bytes.restype = ctypes.c_size_t
     L.bed_forward_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(BedConfig)]
     L.bed_forward_host_f32.restype = ctypes.c_int
@@ -122,9 +122,10 @@ def forward_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr, fl
 
 
 def forward_ws_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr, flags_ptr,
-                   cfg: BedConfig, ws_ptr, ws_bytes: int, stream: int) -> None:
+                   diag_ptr, resid_ptr, cfg: BedConfig, ws_ptr, ws_bytes: int, stream: int) -> None:
     rc = lib().bed_forward_ws_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr,
-                                  flags_ptr, ctypes.byref(cfg), ws_ptr, ws_bytes, stream)
+                                  flags_ptr, diag_ptr, resid_ptr, ctypes.byref(cfg), ws_ptr,
+                                  ws_bytes, stream)
     check(rc, "bed_forward_ws_f32")
 
 

@@ -66,7 +66,8 @@ class NonFinite(BatchedEigError):
 class NoConvergence(BatchedEigError):
     """Iteration budget exhausted with off-diagonal mass above threshold (core.py:83-93).
 
-    ``residual_offdiag_max`` is NaN when the device path does not report it.
+    ``residual_offdiag_max``: the largest coupling left in any offender's
+    active block, on its power-of-two equilibrated band (qr.py:385-389).
     """
 
     def __init__(self, batch_indices, residual_offdiag_max: float):
@@ -229,10 +230,17 @@ class SolverConfig:
 class SolveDiagnostics:
     """Counters of one solve (qr.py:101-118).
 
-    With per-matrix gating every matrix has its own loop: ``converged_steps``
-    holds each matrix's double-step count and ``double_steps`` their maximum.
-    ``reductions`` / ``reduction_events`` / ``rotation_count`` describe the
-    batch-gated reference loop and are reported as -1 by the device path.
+    With per-matrix gating every matrix runs its own loop, so the reference's
+    counters exist per matrix (``bed_forward_ws_f32``'s ``diag`` output):
+    ``converged_steps`` holds each matrix's double-step count,
+    ``rotations`` the rotations applied to it (sum of active - 1 over its
+    sweeps), ``reduction_counts`` its trailing deflations.  The scalar fields
+    pool them over the batch and equal the reference's for a batch of one:
+    ``double_steps`` the largest step count, ``rotation_count`` and
+    ``reduction_events`` the totals, ``reductions`` the mean number of
+    reductions at the start of a double step over all executed double steps
+    (the reference's step_r_sum / double_steps, qr.py:578).  -1 where a solve
+    did not collect them.
     """
 
     double_steps: int
@@ -240,6 +248,8 @@ class SolveDiagnostics:
     reduction_events: int
     rotation_count: int
     converged_steps: Any = None
+    rotations: Any = None
+    reduction_counts: Any = None
 
 
 @dataclass(frozen=True)

@@ -153,8 +153,8 @@ size_t bed_forward_workspace_bytes(int64_t batch, int32_t n, const bed_config* c
 }
 
 int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,
-                       int32_t* status, int32_t* steps, int32_t* flags, const bed_config* cfg,
-                       void* workspace, size_t workspace_bytes, void* stream) {
+                       int32_t* status, int32_t* steps, int32_t* flags, int32_t* diag, float* resid,
+                       const bed_config* cfg, void* workspace, size_t workspace_bytes, void* stream) {
   int rc = check_forward(A, batch, n, evals, evecs, cfg);
   if (rc) return rc;
   const bool vecs = cfg->compute_vectors != 0;
@@ -162,7 +162,8 @@ int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, f
   if (batch > 0 && n > 8 &&
       (!workspace || bed::split_chunk(batch, n, vecs, k.max_steps, workspace_bytes) == 0))
     return BED_ERR_INVALID_ARGUMENT;  // below bed_forward_workspace_bytes(32, n, cfg)
-  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0) return BED_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0 || !aligned4(diag) || !aligned4(resid))
+    return BED_ERR_MISALIGNED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (flags) {
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
@@ -170,7 +171,7 @@ int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, f
   }
   if (batch == 0) return BED_SUCCESS;
   bed::FwdArgs a{A, batch, n, evals, vecs ? evecs : nullptr, status, steps, flags, k, s,
-                 workspace, workspace_bytes};
+                 bed::DiagOut{diag, resid}, workspace, workspace_bytes};
   cudaError_t e = dispatch_forward(a);
   if (e != cudaSuccess) return cuda_fail(e, "bed_forward_ws_f32 launch");
   return BED_SUCCESS;
@@ -182,8 +183,8 @@ int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, floa
   int rc = check_forward(A, batch, n, evals, evecs, cfg);
   if (rc) return rc;
   if (batch == 0 || n <= 8)
-    return bed_forward_ws_f32(A, batch, n, evals, evecs, status, steps, flags, cfg, nullptr, 0,
-                              stream);
+    return bed_forward_ws_f32(A, batch, n, evals, evecs, status, steps, flags, nullptr, nullptr, cfg,
+                              nullptr, 0, stream);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool vecs = cfg->compute_vectors != 0;
   const int max_steps = kernel_cfg(cfg, n).max_steps;
@@ -198,7 +199,8 @@ int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, floa
     e = pool_alloc(&ws, bytes, s);
   }
   if (e != cudaSuccess) return cuda_fail(e, "bed_forward_f32 workspace");
-  rc = bed_forward_ws_f32(A, batch, n, evals, evecs, status, steps, flags, cfg, ws, bytes, stream);
+  rc = bed_forward_ws_f32(A, batch, n, evals, evecs, status, steps, flags, nullptr, nullptr, cfg, ws,
+                          bytes, stream);
   e = cudaFreeAsync(ws, s);
   if (rc == BED_SUCCESS && e != cudaSuccess) return cuda_fail(e, "bed_forward_f32 free");
   return rc;
@@ -319,7 +321,7 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
     // solve: after this chunk's input arrived and slot b's outputs were read back
     if ((e = cudaStreamWaitEvent(st[C], ev[H][b], 0)) != cudaSuccess ||
         (used[b] && (e = cudaStreamWaitEvent(st[C], ev[D][b], 0)) != cudaSuccess)) { out = cuda_fail(e, "wait"); break; }
-    bed::FwdArgs a{dA, m, n, dL, dV, dS, dK, nullptr, kernel_cfg(cfg, n), st[C],
+    bed::FwdArgs a{dA, m, n, dL, dV, dS, dK, nullptr, kernel_cfg(cfg, n), st[C], bed::DiagOut{nullptr, nullptr},
                    wsb ? pool + slot * kSlots : nullptr, wsb};
     if ((e = dispatch_forward(a)) != cudaSuccess) { out = cuda_fail(e, "bed_forward_host_f32 launch"); break; }
     if ((e = cudaEventRecord(ev[C][b], st[C])) != cudaSuccess) { out = cuda_fail(e, "record"); break; }

@@ -32,6 +32,26 @@ constexpr int kStatusNonPositive = 4;
 // denormal range so 1/scale stays finite).
 constexpr float kZeroTail = 1e-30f;
 
+// Optional per-matrix diagnostics (the reference's SolveDiagnostics counters,
+// qr.py:101-118, _kernels.py:396-398, per matrix): diag[3 j + 0] rotations
+// applied (sum of active - 1 over the matrix's sweeps), [3 j + 1] reduction
+// events (trailing deflations), [3 j + 2] step_r_sum (reductions so far,
+// summed over its double steps); resid[j] the largest active coupling left
+// when the step budget ran out (0 otherwise; NoConvergence's
+// residual_offdiag_max, qr.py:385-389).  Either pointer may be null.
+struct DiagOut {
+  int32_t* diag;
+  float* resid;
+  __device__ __forceinline__ void put(int64_t j, int rot, int red, int srs, float res) const {
+    if (diag) {
+      diag[3 * j] = rot;
+      diag[3 * j + 1] = red;
+      diag[3 * j + 2] = srs;
+    }
+    if (resid) resid[j] = res;
+  }
+};
+
 struct KernelCfg {
   float eps;       // deflation_tol
   float sym_tol;   // symmetry_tol

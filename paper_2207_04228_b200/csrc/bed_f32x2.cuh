@@ -62,4 +62,19 @@ __device__ __forceinline__ void rot2(f2& X, f2& Y, float c, float s, float ns) {
   Y = ffma2(x, f2_bc(s), fmul2(y, f2_bc(c)));
 }
 
+// rot2 written as one in-place asm block (the same four packed operations,
+// same rounding): the outputs reuse the input registers, which keeps the
+// register allocator from inserting moves at the joins of conditionally
+// executed rotation blocks (bed_fold_tma.cuh).
+__device__ __forceinline__ void rot2_ip(f2& X, f2& Y, float c, float s, float ns) {
+  asm("{\n\t.reg .b64 t1, t2, cc, ss, nn;\n\t"
+      "mov.b64 cc, {%2, %2};\n\tmov.b64 ss, {%3, %3};\n\tmov.b64 nn, {%4, %4};\n\t"
+      "mul.rn.f32x2 t1, %1, nn;\n\t"
+      "mul.rn.f32x2 t2, %1, cc;\n\t"
+      "fma.rn.f32x2 %1, %0, ss, t2;\n\t"
+      "fma.rn.f32x2 %0, %0, cc, t1;\n\t}"
+      : "+l"(X.r), "+l"(Y.r)
+      : "f"(c), "f"(s), "f"(ns));
+}
+
 }  // namespace bed

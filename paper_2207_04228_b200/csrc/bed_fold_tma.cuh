@@ -53,7 +53,7 @@ struct FTParams {
   static constexpr size_t BYTES = sizeof(float) * (size_t)TOTAL;
   static_assert(R * LF == NMAX && (R % 2 == 0 || R == 1), "row split");
   static_assert(FT % 32 == 0 && 32 % MPC == 0, "CTA = whole warps, one band warp's lanes");
-  static_assert((MPC * 8) % 16 == 0, "bulk copies move multiples of 16 bytes");
+  static_assert(MPC % 4 == 0 && NW <= 8, "active sizes read as words; fold-warp extents packed in 8 bytes");
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -148,21 +148,37 @@ __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
     int* hdr = reinterpret_cast<int*>(smem + P::OFF_HDR);
 #pragma unroll 1
     for (int s0 = 0; s0 < nrec; s0 += 32) {
-      const int mw_l = s0 + lane < nrec ? __ldg(msw + s0 + lane) : 0;  // 32 sweeps per load
-      int ml_next = lane < MPC ? mls[(size_t)s0 * 32 + lane] : 0;
+      // lane k fetches sweep s0 + k's metadata once per 32 sweeps: the warp's
+      // extent and the active sizes of this CTA's MPC matrices, from which it
+      // forms each fold warp's extent (NW bytes packed in two words)
+      const int sk = s0 + lane;
+      const int mw_l = sk < nrec ? __ldg(msw + sk) : 0;
+      uint32_t wpk[2] = {0u, 0u};
+      if (sk < nrec) {
+        uint8_t ml[MPC];
+#pragma unroll
+        for (int q = 0; q < MPC; q += 4) {
+          const uint32_t wd = __ldg(reinterpret_cast<const uint32_t*>(mls + (size_t)sk * 32 + q));
+          ml[q] = wd & 0xff; ml[q + 1] = (wd >> 8) & 0xff; ml[q + 2] = (wd >> 16) & 0xff; ml[q + 3] = wd >> 24;
+        }
+#pragma unroll
+        for (int f = 0; f < P::NW; ++f) {
+          int mx = 0;
+#pragma unroll
+          for (int k = 0; k < MPC; ++k)
+            if (k >= (32 * f) / LF && k <= (32 * f + 31) / LF) mx = max(mx, (int)ml[k]);
+          wpk[f / 4] |= (uint32_t)mx << (8 * (f % 4));
+        }
+      }
 #pragma unroll 1
       for (int s = s0; s < min(nrec, s0 + 32); ++s) {
         const int b = s % NB;
-        const int ml = ml_next;
-        if (s + 1 < nrec && lane < MPC) ml_next = mls[(size_t)(s + 1) * 32 + lane];
         const int mw = __shfl_sync(0xffffffffu, mw_l, s - s0);
         const int np = min(POS, (mw - 1 + kFoldBlk - 1) / kFoldBlk * kFoldBlk);
         if (s >= NB) mbar_wait(empty + b, ((s / NB) & 1) ^ 1);
+        if (lane == s - s0) {
 #pragma unroll
-        for (int f = 0; f < P::NW; ++f) {
-          const int lo = (32 * f) / LF, hi = (32 * f + 31) / LF;
-          const int wmf = __reduce_max_sync(0xffffffffu, (lane >= lo && lane <= hi) ? ml : 0);
-          if (lane == 0) hdr[b * P::NW + f] = wmf;
+          for (int f = 0; f < P::NW; ++f) hdr[b * P::NW + f] = (wpk[f / 4] >> (8 * (f % 4))) & 0xff;
         }
         __syncwarp();
         if (lane == 0) {  // rows 0 .. np-1 of the sweep record: one contiguous bulk copy
@@ -228,7 +244,7 @@ __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
             } else {
 #pragma unroll
               for (int rp = 0; rp < RP; ++rp)
-                rot2(v[rp][p], v[rp][p + 1], cs[p - p0].x, cs[p - p0].y, -cs[p - p0].y);
+                rot2_ip(v[rp][p], v[rp][p + 1], cs[p - p0].x, cs[p - p0].y, -cs[p - p0].y);
             }
           }
         }

@@ -20,6 +20,7 @@ struct FwdArgs {
   int32_t* flags;
   KernelCfg cfg;
   cudaStream_t stream;
+  DiagOut dg;       // optional per-matrix diagnostics
   void* ws;         // n >= 9: device workspace (bed_forward_workspace_bytes)
   size_t ws_bytes;  // a smaller workspace solves the batch in chunks
 };

@@ -9,10 +9,10 @@ static cudaError_t go_small(const FwdArgs& a) {
   const unsigned grid = (unsigned)((a.batch + kSmallThreads - 1) / kSmallThreads);
   if (a.evecs)
     bed_small_kernel<N, true><<<grid, kSmallThreads, 0, a.stream>>>(
-        a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg);
+        a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg);
   else
     bed_small_kernel<N, false><<<grid, kSmallThreads, 0, a.stream>>>(
-        a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg);
+        a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg);
   return cudaGetLastError();
 }
 

@@ -214,7 +214,8 @@ template <int N, bool VECS>
 __global__ void __launch_bounds__(kSmallThreads)
     bed_small_kernel(const float* __restrict__ A, int64_t batch, float* __restrict__ evals,
                      float* __restrict__ evecs, int32_t* __restrict__ status_out,
-                     int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg) {
+                     int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg,
+                     DiagOut dg) {
   using Lay = SmallLayout<N>;
   constexpr int NN = Lay::NN;
   constexpr int NP = Lay::NP;
@@ -389,7 +390,8 @@ __global__ void __launch_bounds__(kSmallThreads)
   }
 
   // ---- double-shift QR with per-matrix deflation, warp-synchronous
-  int steps = 0;
+  int steps = 0, rot = 0, srs = 0, mfin = N < 2 ? 2 : N;
+  float res_out = 0.0f;
   if constexpr (N >= 3) {
     if constexpr (N <= kUnmaskedMaxN) {
       int m = small_deflate_zero<N>(e, N, cfg.eps);
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kSmallThreads)
             float resid = 0.0f;
 #pragma unroll
             for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
+            res_out = resid;
             if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
             run = false;  // lock the diagonal; the leading 2x2 still closes below
 #pragma unroll
@@ -417,13 +420,17 @@ __global__ void __launch_bounds__(kSmallThreads)
         float lo, hi;
         wilkinson_shifts(ta, tb, td, lo, hi);
         small_sweep_full<N, VECS>(d, e, v, run, run ? hi : 0.0f);
+        srs += run ? N - m : 0;
+        rot += run ? m - 1 : 0;
         m = small_deflate_zero<N>(e, m, cfg.eps);
         const bool on2 = run && m > 2;
         small_sweep_full<N, VECS>(d, e, v, on2, on2 ? lo : 0.0f);
+        rot += on2 ? m - 1 : 0;
         m = small_deflate_zero<N>(e, m, cfg.eps);
         steps += run ? 1 : 0;
         run = run && m > 2;
       }
+      mfin = m;
     } else {
       int m = small_deflate<N>(e, N, cfg.eps);
       bool run = m > 2;
@@ -433,6 +440,7 @@ __global__ void __launch_bounds__(kSmallThreads)
             float resid = 0.0f;
 #pragma unroll
             for (int j = 0; j < N - 1; ++j) resid = fmaxf(resid, j < m - 1 ? fabsf(e[j]) : 0.0f);
+            res_out = resid;
             if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
             run = false;  // lock the diagonal; the leading 2x2 still closes below
           }
@@ -453,12 +461,16 @@ __global__ void __launch_bounds__(kSmallThreads)
         // finished lanes sweep nothing (m = 0); their couplings do not
         // move, so the unconditional deflations leave their m unchanged
         small_sweep<N, VECS>(d, e, v, run ? m : 0, hi);
+        srs += run ? N - m : 0;
+        rot += run ? m - 1 : 0;
         m = small_deflate<N>(e, m, cfg.eps);
         small_sweep<N, VECS>(d, e, v, (run && m > 2) ? m : 0, lo);
+        rot += (run && m > 2) ? m - 1 : 0;
         m = small_deflate<N>(e, m, cfg.eps);
         steps += run ? 1 : 0;
         run = run && m > 2;
       }
+      mfin = m;
     }
   }
   if constexpr (N >= 2) {
@@ -510,6 +522,7 @@ __global__ void __launch_bounds__(kSmallThreads)
     }
     if (status_out) status_out[base + tid] = status;
     if (steps_out) steps_out[base + tid] = steps;
+    dg.put(base + tid, rot, N >= 2 ? N - mfin : 0, srs, res_out);
   }
   if (flags) {
     unsigned bits = __reduce_or_sync(0xffffffffu, (live && status) ? (1u << status) : 0u);

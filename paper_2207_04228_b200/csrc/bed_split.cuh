@@ -107,7 +107,7 @@ template <int NMAX, bool EXACT, bool VECS>
 __global__ void __launch_bounds__(kQThreads)
     bed_qr_kernel(int64_t bc, int64_t c0, int n_rt, SplitWs ws, float* __restrict__ evals,
                   int32_t* __restrict__ status_out, int32_t* __restrict__ steps_out,
-                  int32_t* __restrict__ flags, KernelCfg cfg) {
+                  int32_t* __restrict__ flags, KernelCfg cfg, DiagOut dg) {
   const int n = EXACT ? NMAX : n_rt;
   const int64_t j = (int64_t)blockIdx.x * kQThreads + threadIdx.x;
   const bool live = j < bc;
@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(kQThreads)
     }
   };
 
-  int steps = 0;
+  int steps = 0, rot = 0, srs = 0;
+  float res_out = 0.0f;
   int m = qr_deflate<NMAX>(e, n, cfg.eps);
   bool run = live && m > 2;
   while (__any_sync(0xffffffffu, run)) {
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(kQThreads)
       float resid = 0.0f;
 #pragma unroll
       for (int i = 0; i < NMAX - 1; ++i) resid = fmaxf(resid, i < m - 1 ? fabsf(e[i]) : 0.0f);
+      res_out = resid;
       if (resid >= cfg.eps && status == kStatusOk) status = kStatusNoConv;
       run = false;  // lock the diagonal; the leading 2x2 still closes below
     }
@@ -181,8 +183,11 @@ __global__ void __launch_bounds__(kQThreads)
     const int mwa = __reduce_max_sync(0xffffffffu, ma);
     qr_sweep<NMAX, VECS>(d, e, ma, hi, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr, mwa);
     record_end(mwa, mwa, ma);
+    srs += run ? n - m : 0;
+    rot += run ? m - 1 : 0;
     if (run) m = qr_deflate<NMAX>(e, m, cfg.eps);
     const int mb = (run && m > 2) ? m : 0;
+    rot += mb > 2 ? mb - 1 : 0;
     const int mwb = __reduce_max_sync(0xffffffffu, mb);
     if (mwb > 2) {
       qr_sweep<NMAX, VECS>(d, e, mb, lo, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr, mwb);
@@ -227,6 +232,7 @@ __global__ void __launch_bounds__(kQThreads)
     }
     if (status_out) status_out[c0 + j] = status;
     if (steps_out) steps_out[c0 + j] = steps;
+    dg.put(c0 + j, rot, n - m, srs, res_out);
   }
   if (flags) {
     unsigned bits = __reduce_or_sync(0xffffffffu, (live && status) ? (1u << status) : 0u);

@@ -46,13 +46,13 @@ cudaError_t run_split(const FwdArgs& a) {
       using FP = FTParams<NMAX>;
       bed_qr_kernel<NMAX, EXACT, true><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0,
                                          a.stream>>>(bc, c0, n, ws, a.evals, a.status, a.steps,
-                                                     a.flags, a.cfg);
+                                                     a.flags, a.cfg, a.dg);
       bed_fold_tma_kernel<NMAX, EXACT><<<(unsigned)((bc + FP::MPC - 1) / FP::MPC), FP::THREADS, FP::BYTES,
                                          a.stream>>>(bc, c0, n, ws, a.evals, a.evecs, a.cfg);
     } else {
       bed_qr_kernel<NMAX, EXACT, false><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0,
                                           a.stream>>>(bc, c0, n, ws, a.evals, a.status, a.steps,
-                                                      a.flags, a.cfg);
+                                                      a.flags, a.cfg, a.dg);
     }
     e = cudaGetLastError();
   }

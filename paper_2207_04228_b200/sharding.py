@@ -116,6 +116,8 @@ def batched_eig_devices(a: torch.Tensor, cfg: SolverConfig | None = None,
     evecs = torch.empty((b, n, n), device=out_dev, dtype=torch.float32) if cfg.compute_vectors else None
     status = torch.empty((b,), device=out_dev, dtype=torch.int32)
     steps = torch.empty((b,), device=out_dev, dtype=torch.int32)
+    diag = torch.empty((b, 3), device=out_dev, dtype=torch.int32)
+    resid = torch.empty((b,), device=out_dev, dtype=torch.float32)
     producer = torch.cuda.current_stream(a.device) if a.is_cuda else None
     consumer = torch.cuda.current_stream(out_dev) if out_dev.type == "cuda" else None
     streams = []
@@ -136,13 +138,17 @@ def batched_eig_devices(a: torch.Tensor, cfg: SolverConfig | None = None,
             lv = torch.empty((hi - lo, n, n), device=dev, dtype=torch.float32) if evecs is not None else None
             ls = torch.empty((hi - lo,), device=dev, dtype=torch.int32)
             lk = torch.empty((hi - lo,), device=dev, dtype=torch.int32)
-            solver.forward_into(local, cfg, le, lv, ls, lk)
+            ld = torch.empty((hi - lo, 3), device=dev, dtype=torch.int32)
+            lr = torch.empty((hi - lo,), device=dev, dtype=torch.float32)
+            solver.forward_into(local, cfg, le, lv, ls, lk, diag=ld, resid=lr)
             evals[lo:hi].copy_(le, non_blocking=True)
             if lv is not None:
                 evecs[lo:hi].copy_(lv, non_blocking=True)
             status[lo:hi].copy_(ls, non_blocking=True)
             steps[lo:hi].copy_(lk, non_blocking=True)
-            for t in (evals, evecs, status, steps):
+            diag[lo:hi].copy_(ld, non_blocking=True)
+            resid[lo:hi].copy_(lr, non_blocking=True)
+            for t in (evals, evecs, status, steps, diag, resid):
                 if t is not None and t.is_cuda:
                     t.record_stream(st)
     for st in streams:
@@ -153,5 +159,5 @@ def batched_eig_devices(a: torch.Tensor, cfg: SolverConfig | None = None,
     flags = 0
     for code in torch.unique(status.cpu()).tolist():
         flags |= (1 << code) if code else 0
-    solver._raise_for_status(a, status, flags, cfg)
-    return EigenResult(evals, evecs, solver._diagnostics(steps))
+    solver._raise_for_status(a, status, flags, cfg, resid)
+    return EigenResult(evals, evecs, solver._diagnostics(steps, diag))

@@ -64,11 +64,13 @@ def workspace(A: torch.Tensor, cfg: SolverConfig, max_bytes: int | None = None) 
 def forward_into(A: torch.Tensor, cfg: SolverConfig, evals: torch.Tensor,
                  evecs: torch.Tensor | None, status: torch.Tensor | None = None,
                  steps: torch.Tensor | None = None, flags: torch.Tensor | None = None,
-                 ws: torch.Tensor | None = None) -> None:
+                 ws: torch.Tensor | None = None, diag: torch.Tensor | None = None,
+                 resid: torch.Tensor | None = None) -> None:
     """Launch the forward on preallocated device tensors, stream-ordered,
     without any host synchronisation (the C ABI call ``bed_forward_ws_f32``).
     The n >= 9 workspace is ``ws`` (from :func:`workspace`) or, when omitted,
-    a fresh one from torch's caching allocator."""
+    a fresh one from torch's caching allocator.  ``diag`` (batch, 3) int32 and
+    ``resid`` (batch,) float32 receive the per-matrix diagnostics."""
     b, n, _ = A.shape
     ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
     if ws is None and n > 8:
@@ -79,11 +81,12 @@ def forward_into(A: torch.Tensor, cfg: SolverConfig, evals: torch.Tensor,
         wb = ws.numel() - (wp - ws.data_ptr())
     _native.forward_ws_f32(A.data_ptr(), b, n, evals.data_ptr(),
                            ptr(evecs) if cfg.compute_vectors else None,
-                           ptr(status), ptr(steps), ptr(flags),
+                           ptr(status), ptr(steps), ptr(flags), ptr(diag), ptr(resid),
                            _native.make_config(cfg, n), wp or None, wb, _stream_handle(A.device))
 
 
-def _raise_for_status(A: torch.Tensor, status: torch.Tensor, flags: int, cfg: SolverConfig) -> None:
+def _raise_for_status(A: torch.Tensor, status: torch.Tensor, flags: int, cfg: SolverConfig,
+                      resid: torch.Tensor | None = None) -> None:
     """Map per-matrix status codes onto the reference exceptions.
 
     Order follows the reference: validate (finiteness over the whole batch
@@ -103,10 +106,10 @@ def _raise_for_status(A: torch.Tensor, status: torch.Tensor, flags: int, cfg: So
         raise NonSymmetric(k, float((a - a.T).abs().max()))
     if cfg.strict_convergence and flags & (1 << _native.STATUS_NO_CONVERGENCE):
         idx = torch.nonzero(st == _native.STATUS_NO_CONVERGENCE)[:, 0].tolist()
-        raise NoConvergence(idx, float("nan"))
+        raise NoConvergence(idx, float(resid.max()) if resid is not None else float("nan"))
 
 
-def _solve_device(A: torch.Tensor, cfg: SolverConfig, check: bool = True):
+def _solve_device(A: torch.Tensor, cfg: SolverConfig, check: bool = True, diagnostics: bool = False):
     A = _check_cuda_f32(A, "A")
     b, n, _ = A.shape
     dev = A.device
@@ -115,17 +118,48 @@ def _solve_device(A: torch.Tensor, cfg: SolverConfig, check: bool = True):
     status = torch.empty((b,), device=dev, dtype=torch.int32)
     steps = torch.empty((b,), device=dev, dtype=torch.int32)
     flags = torch.empty((1,), device=dev, dtype=torch.int32)
+    diag = torch.empty((b, 3), device=dev, dtype=torch.int32) if diagnostics else None
+    resid = torch.empty((b,), device=dev, dtype=torch.float32) if diagnostics or check else None
     with torch.cuda.device(dev):
-        forward_into(A, cfg, evals, evecs, status, steps, flags)
+        forward_into(A, cfg, evals, evecs, status, steps, flags, diag=diag, resid=resid)
     if check:
-        _raise_for_status(A, status, int(flags.item()), cfg)
-    return evals, evecs, status, steps
+        _raise_for_status(A, status, int(flags.item()), cfg, resid)
+    return evals, evecs, status, steps, diag
 
 
-def _diagnostics(steps) -> SolveDiagnostics:
+def _diagnostics(steps, diag=None) -> SolveDiagnostics:
+    """Pool the per-matrix counters (see SolveDiagnostics)."""
     k = int(steps.max()) if len(steps) else 0
-    return SolveDiagnostics(double_steps=k, reductions=-1.0, reduction_events=-1,
-                            rotation_count=-1, converged_steps=steps)
+    if diag is None:
+        return SolveDiagnostics(double_steps=k, reductions=-1.0, reduction_events=-1,
+                                rotation_count=-1, converged_steps=steps)
+    if isinstance(diag, np.ndarray):
+        tot = diag.astype(np.int64).sum(axis=0).tolist() if len(diag) else [0, 0, 0]
+        nsteps = int(steps.astype(np.int64).sum())
+    else:
+        tot = diag.long().sum(dim=0).tolist() if len(diag) else [0, 0, 0]
+        nsteps = int(steps.long().sum()) if len(steps) else 0
+    return SolveDiagnostics(double_steps=k, reductions=tot[2] / nsteps if nsteps else 0.0,
+                            reduction_events=int(tot[1]), rotation_count=int(tot[0]),
+                            converged_steps=steps, rotations=diag[:, 0],
+                            reduction_counts=diag[:, 1])
+
+
+def _validate_host(a: np.ndarray, cfg: SolverConfig) -> np.ndarray:
+    """The reference ``validate`` (core.py:286-309) on a float64 host batch:
+    NonFinite at the first non-finite entry, NonSymmetric when max|a - a^T| >
+    symmetry_tol * max(1, ||A||_F), else (A + A^T) / 2."""
+    finite = np.isfinite(a)
+    if not finite.all():
+        b, i, j = (int(x) for x in np.argwhere(~finite)[0])
+        raise NonFinite(b, (i, j))
+    at = a.transpose(0, 2, 1)
+    asym = np.abs(a - at).max(axis=(1, 2))
+    bad = asym > cfg.symmetry_tol * np.maximum(1.0, np.linalg.norm(a, axis=(1, 2)))
+    if bad.any():
+        k = int(np.argmax(bad))
+        raise NonSymmetric(k, float(asym[k]))
+    return (a + at) / 2.0
 
 
 def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
@@ -145,21 +179,25 @@ def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
     if isinstance(data, torch.Tensor):
         if data.ndim != 3 or data.shape[1] != data.shape[2] or data.shape[0] < 1:
             raise ShapeMismatch(f"expected (batch, n, n) tensor, got {tuple(data.shape)}")
-        evals, evecs, status, steps = _solve_device(data, cfg)
-        return EigenResult(evals, evecs, _diagnostics(steps))
+        evals, evecs, status, steps, diag = _solve_device(data, cfg, diagnostics=True)
+        return EigenResult(evals, evecs, _diagnostics(steps, diag))
     arr = np.asarray(data)
     if arr.ndim != 3 or arr.shape[1] != arr.shape[2] or arr.shape[0] < 1:
         raise ShapeMismatch(f"expected (batch, n, n) array, got {arr.shape}")
+    if arr.dtype != np.float32:
+        # validate + symmetrise in the caller's precision before the FP32 cast
+        # (core.py:286-309): rounding to FP32 can split a_ij and a_ji by an ulp
+        arr = _validate_host(np.asarray(arr, dtype=np.float64), cfg)
     host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).pin_memory()
     dev = torch.device("cuda", torch.cuda.current_device())
     A = host.to(dev, non_blocking=True)
-    evals, evecs, status, steps = _solve_device(A, cfg)
+    evals, evecs, status, steps, diag = _solve_device(A, cfg, diagnostics=True)
     out_l = evals.to("cpu", non_blocking=True)
     out_v = evecs.to("cpu", non_blocking=True) if evecs is not None else None
     torch.cuda.current_stream(dev).synchronize()
     return EigenResult(out_l.numpy().astype(np.float64),
                        None if out_v is None else out_v.numpy().astype(np.float64),
-                       _diagnostics(steps.cpu().numpy()))
+                       _diagnostics(steps.cpu().numpy(), diag.cpu().numpy()))
 
 
 def taylor_backward(V: torch.Tensor, evals: torch.Tensor, g_v: torch.Tensor | None,
@@ -212,7 +250,7 @@ class BatchedEigFn(torch.autograd.Function):
         cfg = cfg or SolverConfig()
         if not cfg.compute_vectors:
             raise ValueError("the differentiable ED needs compute_vectors=True")
-        evals, evecs, _, _ = _solve_device(A.detach(), cfg, check=check)
+        evals, evecs, _, _, _ = _solve_device(A.detach(), cfg, check=check)
         ctx.save_for_backward(evals, evecs)
         ctx.degree = degree
         ctx.check = check

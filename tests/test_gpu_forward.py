@@ -315,3 +315,65 @@ def test_headline_inputs_c2(bed):
     o = oracle.forward(a[idx].double().cpu().numpy())
     assert np.all(P.eig_err(lam[idx].cpu().numpy(), o.eigenvalues) <= P.EIG_TOL)
     assert np.all(P.vector_err(v[idx].cpu().numpy(), o.eigenvectors, o.eigenvalues) <= 1.0)
+
+
+def test_float64_host_input_validated_before_the_fp32_cast(bed):
+    """A float64 batch symmetric to ~1e-16 (accepted by the reference) can
+    round a_ij and a_ji to adjacent FP32 values: it is symmetrised in float64
+    first, so it solves; a real asymmetry is still rejected with the
+    reference's fields (core.py:286-309)."""
+    a = oracle.gen_spd(64, 6, 6)
+    # put a_01 / a_10 on either side of an FP32 rounding midpoint: a float64
+    # asymmetry of ~1e-16 relative that rounds to two adjacent FP32 values
+    x = a[:, 0, 1].astype(np.float32)
+    mid = (x.astype(np.float64) + np.nextafter(x, np.float32(np.inf)).astype(np.float64)) / 2
+    a[:, 0, 1] = mid * (1 - 1e-15)
+    a[:, 1, 0] = mid * (1 + 1e-15)
+    assert np.abs(a - a.transpose(0, 2, 1)).max() < 1e-12
+    assert np.abs(a.astype(np.float32) - a.astype(np.float32).transpose(0, 2, 1)).max() > 0
+    r = bed.batched_eig(bed.BatchedSymmetric(a), bed.SolverConfig(**VERIFY, max_double_steps=24))
+    o = oracle.forward((a + a.transpose(0, 2, 1)) / 2)
+    assert np.all(P.eig_err(r.eigenvalues, o.eigenvalues) <= P.EIG_TOL)
+    bad = a.copy()
+    bad[5, 0, 3] += 1e-3
+    with pytest.raises(bed.NonSymmetric) as err:
+        bed.batched_eig(bed.BatchedSymmetric(bad))
+    assert err.value.batch_index == 5
+    bad = a.copy()
+    bad[9, 2, 1] = np.inf
+    with pytest.raises(bed.NonFinite) as err:
+        bed.batched_eig(bed.BatchedSymmetric(bad))
+    assert err.value.batch_index == 9 and err.value.position == (2, 1)
+
+
+@pytest.mark.parametrize("n", [4, 6, 12, 16, 24, 40])
+def test_diagnostics_match_the_per_matrix_reference_loop(bed, n):
+    """Per-matrix SolveDiagnostics counters (qr.py:101-118) against the
+    oracle's restatement of the reference loop gated per matrix, at the
+    reference's default tolerance (1e-5, above the FP32 floor)."""
+    b = 96
+    a = oracle.gen_spd(b, n, 500 + n).astype(np.float32)
+    cfg = bed.SolverConfig(deflation_tol=1e-5, max_double_steps=4 * n)
+    r = bed.batched_eig(torch.from_numpy(a).cuda(), cfg)
+    d = r.diagnostics
+    o = oracle.forward(a.astype(np.float64), deflation_tol=1e-5, max_double_steps=4 * n)
+    steps = d.converged_steps.cpu().numpy()
+    rots = d.rotations.cpu().numpy()
+    reds = d.reduction_counts.cpu().numpy()
+    # FP32 vs float64 can move a deflation by one sweep on a few matrices
+    assert np.mean(steps == o.double_steps) >= 0.9
+    assert np.mean(rots == o.rotations) >= 0.9
+    assert np.all(reds == n - 2)  # every matrix converged down to its closing 2x2
+    assert d.rotation_count == int(rots.sum()) and d.reduction_events == int(reds.sum())
+    assert d.double_steps == int(steps.max())
+    assert 0.0 < d.reductions < n - 2
+
+
+def test_no_convergence_reports_the_residual(bed):
+    hard = oracle.gen_spd(64, 16, 5).astype(np.float32)
+    with pytest.raises(bed.NoConvergence) as err:
+        bed.batched_eig(torch.from_numpy(hard).cuda(),
+                        bed.SolverConfig(deflation_tol=3e-12, max_double_steps=1))
+    res = err.value.residual_offdiag_max
+    assert np.isfinite(res) and res >= 2.0 ** -22
+    assert len(err.value.batch_indices) > 0

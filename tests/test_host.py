@@ -46,7 +46,7 @@ def test_abi_argument_checks_need_no_gpu():
     w32 = _native.workspace_bytes(32, 16, c16)
     assert 0 < w32 < _native.workspace_bytes(64, 16, c16) < _native.workspace_bytes(1 << 20, 16, c16)
     # below the 32-matrix minimum: rejected before any CUDA call
-    assert L.bed_forward_ws_f32(1 << 20, 100, 16, 1 << 20, 1 << 20, None, None, None, ctypes.byref(c16),
+    assert L.bed_forward_ws_f32(1 << 20, 100, 16, 1 << 20, 1 << 20, None, None, None, None, None, ctypes.byref(c16),
                                 1 << 20, w32 - 1, None) == 1
     bad = _native.BedConfig(1e-5, 1e-12, 8, 7, 1, 0)  # bad sort code
     assert L.bed_forward_f32(None, 0, 4, None, None, None, None, None, ctypes.byref(bad), None) == 1
