@@ -325,6 +325,8 @@ def run_ours(args):
     }
     mean_steps = float(step.steps.float().mean())
     line["config"]["mean_double_steps"] = mean_steps
+    line["config"]["qr_useful_lane_frac"] = float(
+        mean_steps / step.steps.float().view(-1, 32).max(dim=1).values.mean())
     line["config"]["max_double_steps_used"] = int(step.steps.max())
     if world > 1:
         dist.barrier()
@@ -364,23 +366,39 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def torch_eigh_ms(torch, a, reps=3):
+def torch_eigh_ms(torch, a, reps=3, chunk=1 << 16):
     """torch.linalg.eigh (cuSOLVER batched syevj, FP32) on the same resident
-    batch: CUDA-event time per call, best of `reps` after one warm call."""
-    try:
-        torch.linalg.eigh(a)
-        torch.cuda.synchronize()
-        best = float("inf")
-        for _ in range(reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+    batch, CUDA-event time per full pass (best of `reps`; one pass when a
+    pass takes over half a second).  Batches cuSOLVER rejects whole are
+    passed in chunks of 65536 matrices inside the timed region."""
+
+    def run(chunked):
+        if not chunked:
             torch.linalg.eigh(a)
-            e1.record()
+            return
+        for lo in range(0, a.shape[0], chunk):
+            torch.linalg.eigh(a[lo:lo + chunk])
+
+    for chunked in (False, True):
+        try:
+            best = float("inf")
+            for r in range(reps + 1):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run(chunked)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1)
+                if r > 0 or ms > 500.0:
+                    best = min(best, ms)
+                if ms > 500.0:
+                    break
+            return best
+        except Exception:  # noqa: BLE001
             torch.cuda.synchronize()
-            best = min(best, e0.elapsed_time(e1))
-        return best
-    except Exception:  # noqa: BLE001
-        return None
+            torch.cuda.empty_cache()
+    return None
 
 
 def other_configs(torch, bed, dev, hbm_peak):
@@ -399,9 +417,13 @@ def other_configs(torch, bed, dev, hbm_peak):
         # size can pay one-off costs (module load, workspace pool growth)
         sec = min(time_steps(torch, st, reps, 5) for _ in range(3)) / reps
         bound, frac, _, _ = roofline(n, mode, b, sec, hbm_peak)
+        stp = st.steps.float()
+        wmax = stp[: b // 32 * 32].view(-1, 32).max(dim=1).values.mean() if b >= 32 else stp.max()
         row = {"n": n, "batch": b, "mode": mode, "ms": sec * 1e3, "value": b / sec,
                "roofline_bound": bound, "roofline_frac": frac,
-               "mean_double_steps": float(st.steps.float().mean())}
+               "mean_double_steps": float(stp.mean()),
+               # warp-synchronous QR: lanes idle once their matrix is done
+               "qr_useful_lane_frac": float(stp.mean() / wmax)}
         if mode == "fwd":
             te = torch_eigh_ms(torch, st.a)
             row["torch_eigh_ms"] = te

@@ -149,7 +149,8 @@ const char* bed_last_cuda_error(void) { return g_last_cuda; }
 size_t bed_forward_workspace_bytes(int64_t batch, int32_t n, const bed_config* cfg) {
   if (!cfg || batch <= 0 || n <= 8 || n > 64) return 0;
   const bed::KernelCfg k = kernel_cfg(cfg, n);
-  return bed::split_plan((batch + 31) / 32 * 32, n, cfg->compute_vectors != 0, k.max_steps).bytes;
+  const bool vecs = cfg->compute_vectors != 0;
+  return bed::split_plan((batch + 31) / 32 * 32, n, vecs, k.max_steps).bytes;
 }
 
 int bed_forward_ws_f32(const float* A, int64_t batch, int32_t n, float* evals, float* evecs,

@@ -11,15 +11,7 @@
 
 namespace bed {
 
-template <int NMAX, bool EXACT>
-cudaError_t run_split(const FwdArgs& a) {
-  const bool vecs = a.evecs != nullptr;
-  const int n = a.n;
-  const int64_t nn = (int64_t)n * n;
-  const int64_t Bc = split_chunk(a.batch, n, vecs, a.cfg.max_steps, a.ws_bytes);
-  if (Bc == 0 || a.ws == nullptr) return cudaErrorInvalidValue;
-  const SplitPlan pl = split_plan(Bc, n, vecs, a.cfg.max_steps);
-  char* base = static_cast<char*>(a.ws);
+inline SplitWs split_ws(char* base, const SplitPlan& pl, bool vecs, int max_steps) {
   SplitWs ws;
   ws.P = vecs ? reinterpret_cast<float*>(base + pl.oP) : nullptr;
   ws.D = reinterpret_cast<float*>(base + pl.oD);
@@ -30,31 +22,58 @@ cudaError_t run_split(const FwdArgs& a) {
   ws.msw = vecs ? reinterpret_cast<int32_t*>(base + pl.oM) : nullptr;
   ws.nsw = vecs ? reinterpret_cast<int32_t*>(base + pl.oN) : nullptr;
   ws.mlane = vecs ? reinterpret_cast<uint8_t*>(base + pl.oML) : nullptr;
-  ws.Bc = Bc;
-  ws.Smax = 2 * a.cfg.max_steps + 1;
-  cudaError_t e = cudaSuccess;
+  ws.Bc = pl.Bc;
+  ws.Smax = 2 * max_steps + 1;
+  return ws;
+}
 
+// H for matrices [c0, c0 + bc) on stream st.
+template <int NMAX, bool EXACT>
+cudaError_t launch_h(const FwdArgs& a, const SplitWs& ws, int64_t c0, int64_t bc, cudaStream_t st) {
+  const bool vecs = a.evecs != nullptr;
   using HP = HHParams<NMAX>;
   auto hk = vecs ? bed_hh_kernel<NMAX, EXACT, true> : bed_hh_kernel<NMAX, EXACT, false>;
-  e = ensure_smem(hk, HP::BYTES);
+  hk<<<(unsigned)((bc + HP::G - 1) / HP::G), HP::THREADS, HP::BYTES, st>>>(a.A + c0 * a.n * a.n, bc,
+                                                                            a.n, ws, a.cfg);
+  return cudaGetLastError();
+}
+
+// Q (+ F with vectors) for matrices [c0, c0 + bc) on stream st.
+template <int NMAX, bool EXACT>
+cudaError_t launch_qf(const FwdArgs& a, const SplitWs& ws, int64_t c0, int64_t bc, cudaStream_t st) {
+  const int n = a.n;
+  if (a.evecs != nullptr) {
+    using FP = FTParams<NMAX>;
+    bed_qr_kernel<NMAX, EXACT, true><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0, st>>>(
+        bc, c0, n, ws, a.evals, a.status, a.steps, a.flags, a.cfg, a.dg);
+    bed_fold_tma_kernel<NMAX, EXACT><<<(unsigned)((bc + FP::MPC - 1) / FP::MPC), FP::THREADS, FP::BYTES,
+                                       st>>>(bc, c0, n, ws, a.evals, a.evecs, a.cfg);
+  } else {
+    bed_qr_kernel<NMAX, EXACT, false><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0, st>>>(
+        bc, c0, n, ws, a.evals, a.status, a.steps, a.flags, a.cfg, a.dg);
+  }
+  return cudaGetLastError();
+}
+
+template <int NMAX, bool EXACT>
+cudaError_t run_split(const FwdArgs& a) {
+  const bool vecs = a.evecs != nullptr;
+  const int n = a.n;
+  if (a.ws == nullptr) return cudaErrorInvalidValue;
+  using HP = HHParams<NMAX>;
+  cudaError_t e = ensure_smem(vecs ? bed_hh_kernel<NMAX, EXACT, true> : bed_hh_kernel<NMAX, EXACT, false>,
+                              HP::BYTES);
   if (e == cudaSuccess && vecs) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT>, FTParams<NMAX>::BYTES);
+  if (e != cudaSuccess) return e;
+  char* base = static_cast<char*>(a.ws);
+
+  const int64_t Bc = split_chunk(a.batch, n, vecs, a.cfg.max_steps, a.ws_bytes);
+  if (Bc == 0) return cudaErrorInvalidValue;
+  const SplitWs ws = split_ws(base, split_plan(Bc, n, vecs, a.cfg.max_steps), vecs, a.cfg.max_steps);
   for (int64_t c0 = 0; c0 < a.batch && e == cudaSuccess; c0 += Bc) {
     const int64_t bc = std::min<int64_t>(Bc, a.batch - c0);
-    hk<<<(unsigned)((bc + HP::G - 1) / HP::G), HP::THREADS, HP::BYTES, a.stream>>>(
-        a.A + c0 * nn, bc, n, ws, a.cfg);
-    if (vecs) {
-      using FP = FTParams<NMAX>;
-      bed_qr_kernel<NMAX, EXACT, true><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0,
-                                         a.stream>>>(bc, c0, n, ws, a.evals, a.status, a.steps,
-                                                     a.flags, a.cfg, a.dg);
-      bed_fold_tma_kernel<NMAX, EXACT><<<(unsigned)((bc + FP::MPC - 1) / FP::MPC), FP::THREADS, FP::BYTES,
-                                         a.stream>>>(bc, c0, n, ws, a.evals, a.evecs, a.cfg);
-    } else {
-      bed_qr_kernel<NMAX, EXACT, false><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0,
-                                          a.stream>>>(bc, c0, n, ws, a.evals, a.status, a.steps,
-                                                      a.flags, a.cfg, a.dg);
-    }
-    e = cudaGetLastError();
+    e = launch_h<NMAX, EXACT>(a, ws, c0, bc, a.stream);
+    if (e == cudaSuccess) e = launch_qf<NMAX, EXACT>(a, ws, c0, bc, a.stream);
   }
   return e;
 }

@@ -17,6 +17,13 @@ KEYS = [
     "launch__block_size", "smsp__thread_inst_executed_per_inst_executed.ratio",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smsp__warps_eligible.avg.per_cycle_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smsp__pcsamp_warps_issue_stalled_no_instructions",
+    "smsp__pcsamp_warps_issue_stalled_barrier",
+    "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
+    "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
+    "smsp__pcsamp_sample_count",
 ]
 
 
