@@ -31,6 +31,8 @@ from .solver import (  # noqa: F401
     forward_into,
     matrix_power,
     scatter_matrices,
+    spectral_power,
+    SpectralPowerFn,
     taylor_backward,
     workspace,
     zca_whiten,

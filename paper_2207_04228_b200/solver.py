@@ -30,6 +30,7 @@ from .core import (
 )
 
 __all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into", "workspace",
+           "spectral_power", "SpectralPowerFn",
            "matrix_power", "zca_whiten", "scatter_matrices", "TAYLOR_DEGREE"]
 
 TAYLOR_DEGREE = 9
@@ -321,6 +322,69 @@ def scatter_matrices(x: torch.Tensor, eps: float = 0.0) -> torch.Tensor:
         _native.scatter_f32(x.data_ptr(), b, n, m, float(eps), out.data_ptr(),
                             _stream_handle(x.device))
     return out
+
+
+def _power_values(lam: torch.Tensor, p: float, floor: float | None):
+    """f(lambda) = max(lambda, floor)^p and f'(lambda) (0 where the floor
+    clamps), the floor resolved per matrix like bed_matrix_power_f32:
+    None -> 1e-12 * lambda_max (solver.py:131-132)."""
+    lam64 = lam.double()
+    fl = (1e-12 * lam64.max(dim=1, keepdim=True).values) if floor is None else torch.full_like(lam64[:, :1], floor)
+    clamped = lam64 < fl
+    x = torch.where(clamped, fl, lam64)
+    f = x.pow(p)
+    df = torch.where(clamped, torch.zeros_like(x), p * x.pow(p - 1))
+    return f.float(), df.float()
+
+
+class SpectralPowerFn(torch.autograd.Function):
+    """Differentiable spectral power A -> V diag(max(lambda, floor)^p) V^T
+    (the reference matrix_power, solver.py:115-143, composed with the ED):
+    forward = bed_forward + bed_matrix_power_f32; backward through f(lambda):
+    with Y = V f(Lambda) V^T,  gV = (gY + gY^T) V f(Lambda) and
+    gLambda = f'(lambda) o diag(V^T gY V), then the paper's Taylor-K ED
+    backward (bed_backward_f32) maps (gV, gLambda) to gA -- the chain the
+    decorrelated-BN / whitening consumer differentiates."""
+
+    @staticmethod
+    def forward(ctx, A, p: float, cfg: SolverConfig | None = None, floor: float | None = None,
+                degree: int = TAYLOR_DEGREE, check: bool = True):
+        cfg = cfg or SolverConfig()
+        evals, evecs, _, _, _ = _solve_device(A.detach(), cfg, check=check)
+        out = _power_device(evecs, evals, p, floor) if check else _power_nocheck(evecs, evals, p, floor)
+        ctx.save_for_backward(evals, evecs)
+        ctx.p, ctx.floor, ctx.degree, ctx.check = p, floor, degree, check
+        return out
+
+    @staticmethod
+    def backward(ctx, g_out):
+        evals, evecs = ctx.saved_tensors
+        f, df = _power_values(evals, ctx.p, ctx.floor)
+        gs = g_out.float() + g_out.float().transpose(1, 2)
+        g_v = torch.bmm(gs, evecs) * f[:, None, :]
+        m = torch.bmm(evecs.transpose(1, 2), torch.bmm(g_out.float(), evecs))
+        g_l = torch.diagonal(m, dim1=1, dim2=2) * df
+        gA = taylor_backward(evecs, evals, g_v.contiguous(), g_l.contiguous(), ctx.degree, ctx.check)
+        return gA, None, None, None, None, None
+
+
+def _power_nocheck(V, lam, p, floor):
+    V = _check_cuda_f32(V, "eigenvectors")
+    lam = _check_cuda_f32(lam, "eigenvalues")
+    b, n, _ = V.shape
+    out = torch.empty_like(V)
+    with torch.cuda.device(V.device):
+        _native.matrix_power_f32(V.data_ptr(), lam.data_ptr(), out.data_ptr(), None, None, b, n, float(p),
+                                 -1.0 if floor is None else float(floor), _stream_handle(V.device))
+    return out
+
+
+def spectral_power(A: torch.Tensor, p: float, cfg: SolverConfig | None = None,
+                   floor: float | None = None, degree: int = TAYLOR_DEGREE, check: bool = True):
+    """V diag(max(lambda, floor)^p) V^T of a CUDA float32 batch, differentiable
+    in A (see SpectralPowerFn); ``check=False`` keeps forward and backward
+    free of host synchronisation."""
+    return SpectralPowerFn.apply(A, p, cfg, floor, degree, check)
 
 
 def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None) -> BatchedMatrix:

@@ -40,3 +40,31 @@ def test_bench_csv(capsys):
     lines = capsys.readouterr().out.strip().splitlines()
     assert lines[0] == cli.CSV_HEADER
     assert len(lines) == 3 and lines[1].startswith("4,64,full,")
+
+
+def test_bench_csv_counters(capsys):
+    assert cli.main(["bench", "--dims", "12", "--batches", "32", "--reps", "1"]) == 0
+    row = capsys.readouterr().out.strip().splitlines()[1].split(",")
+    mean_r, mean_k, rotations = float(row[5]), float(row[6]), int(row[7])
+    assert 0 < mean_r < 10 and mean_k > 1 and rotations > 32 * 10
+    assert row[8] == ""  # max_eig_err is a verify-run quantity (reference bench.py:71)
+
+
+def test_verify_grid_passes(capsys):
+    rc = cli.main(["verify", "--dims", "4,12,24", "--batches", "1,64", "--count", "128", "--csv"])
+    out = capsys.readouterr().out.strip().splitlines()
+    assert out[0] == "dim,batch,count,max_eig_err,max_recon,max_orth,max_single_dev,r_median,passed"
+    assert len(out) == 7
+    assert rc == cli.EXIT_OK, out
+    for line in out[1:]:
+        f = line.split(",")
+        assert int(f[2]) >= 128 and float(f[3]) <= 1e-5 and f[-1] == "1"
+        assert float(f[6]) == 0.0  # per-matrix deflation: batch and single solves agree exactly
+
+
+def test_verify_table_and_failing_gate(capsys):
+    assert cli.main(["verify", "--dims", "8", "--batches", "16", "--count", "16"]) == cli.EXIT_OK
+    text = capsys.readouterr().out
+    assert "eig_err" in text and "pass" in text
+    # an impossible gate fails the cell and the exit status
+    assert cli.main(["verify", "--dims", "8", "--batches", "16", "--count", "16", "--tol", "1e-30"]) == cli.EXIT_FAIL

@@ -9,6 +9,7 @@ import pytest
 import torch
 
 import oracle
+import parity as P
 
 pytestmark = pytest.mark.gpu
 
@@ -178,3 +179,59 @@ def test_zca_large_batch(bed, n):
     cov = c @ c.transpose(1, 2)
     # eps_reg shrinks the whitened scatter slightly below I
     assert float((cov - torch.eye(n, device="cuda", dtype=torch.float64)).abs().max()) <= 2e-2
+
+
+# ---- backward through f(lambda) (SpectralPowerFn)
+
+
+def _sep_spd(b, n, ratio, seed):
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((b, n, n)))
+    lam = 2.0 * ratio ** np.arange(n)
+    a = (q * lam[None, None, :]) @ q.transpose(0, 2, 1)
+    return ((a + a.transpose(0, 2, 1)) / 2).astype(np.float32)
+
+
+@pytest.mark.parametrize("n,p", [(4, -0.5), (8, 0.5), (16, -0.5), (16, 2.0), (32, -1.0)])
+def test_spectral_power_gradient_matches_exact_autograd_at_large_degree(bed, n, p):
+    """Degree -> large: the Taylor-K chain equals exact float64 autograd of
+    V diag(lambda^p) V^T through torch.linalg.eigh."""
+    b = 24
+    a = _sep_spd(b, n, 0.8 if n <= 16 else 0.9, n)  # condition <= ~30: FP32 error x cond^|p| stays small
+    at = torch.from_numpy(a).cuda().requires_grad_(True)
+    y = bed.spectral_power(at, p, bed.SolverConfig(deflation_tol=3e-12), floor=0.0, degree=300)
+    gy = torch.randn_like(y)
+    (y * gy).sum().backward()
+    ad = torch.from_numpy(a.astype(np.float64)).requires_grad_(True)
+    lam, v = torch.linalg.eigh(ad)
+    yd = (v * lam.pow(p)[:, None, :]) @ v.transpose(1, 2)
+    np.testing.assert_allclose(y.detach().cpu().numpy(), yd.detach().numpy(), rtol=0, atol=1e-4 * float(yd.abs().max()))
+    (yd * gy.double().cpu()).sum().backward()
+    err = P.grad_err(at.grad.cpu().numpy(), ad.grad.numpy())
+    assert err.max() <= 1e-3, err.max()
+
+
+@pytest.mark.parametrize("n", [4, 16, 64])
+def test_spectral_power_gradient_matches_oracle_chain(bed, n):
+    """Degree 9 (the paper's): the same chain restated in float64 --
+    gV = (gY + gY^T) V f, gLambda = f' o diag(V^T gY V), then
+    oracle.taylor_backward."""
+    b, p = 33, -0.5
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((b, n, 4 * n))
+    x = x - x.mean(axis=2, keepdims=True)
+    a = (x @ x.transpose(0, 2, 1) / (4 * n) + 1e-3 * np.eye(n)).astype(np.float32)
+    a = (a + a.transpose(0, 2, 1)) / 2
+    at = torch.from_numpy(a).cuda().requires_grad_(True)
+    y = bed.spectral_power(at, p, bed.SolverConfig(deflation_tol=3e-12), floor=0.0)
+    gy = torch.randn_like(y)
+    (y * gy).sum().backward()
+    r = bed.batched_eig(torch.from_numpy(a).cuda(), bed.SolverConfig(deflation_tol=3e-12))
+    v = r.eigenvectors.cpu().numpy().astype(np.float64)
+    lam = r.eigenvalues.cpu().numpy().astype(np.float64)
+    g = gy.cpu().numpy().astype(np.float64)
+    f, df = lam ** p, p * lam ** (p - 1)
+    gv = ((g + g.transpose(0, 2, 1)) @ v) * f[:, None, :]
+    gl = np.diagonal(v.transpose(0, 2, 1) @ g @ v, axis1=1, axis2=2) * df
+    ref = oracle.taylor_backward(v, lam, gv, gl)
+    assert P.grad_err(at.grad.cpu().numpy(), ref).max() <= 1e-4
