@@ -366,20 +366,21 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def torch_eigh_ms(torch, a, reps=3, chunk=1 << 16):
+def torch_eigh_ms(torch, a, reps=3):
     """torch.linalg.eigh (cuSOLVER batched syevj, FP32) on the same resident
     batch, CUDA-event time per full pass (best of `reps`; one pass when a
     pass takes over half a second).  Batches cuSOLVER rejects whole are
-    passed in chunks of 65536 matrices inside the timed region."""
+    passed in chunks (16384, else 4096 matrices; cusolverDnXsyevBatched rejects
+    32768 and up) inside the timed region."""
 
-    def run(chunked):
-        if not chunked:
+    def run(chunk):
+        if not chunk:
             torch.linalg.eigh(a)
             return
         for lo in range(0, a.shape[0], chunk):
             torch.linalg.eigh(a[lo:lo + chunk])
 
-    for chunked in (False, True):
+    for chunked in (0, 1 << 14, 1 << 12):
         try:
             best = float("inf")
             for r in range(reps + 1):
