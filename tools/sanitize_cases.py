@@ -17,6 +17,15 @@ for n, b in ((3, 130), (4, 131), (8, 129), (9, 37), (13, 41), (16, 161), (24, 70
     bed.batched_eig(a.detach(), bed.SolverConfig(compute_vectors=False, max_double_steps=4 * n))
     bed.matrix_power(bed.EigenResult(lam.detach(), v.detach(), None), -0.5)
     bed.scatter_matrices(torch.randn(7, n, 2 * n + 3, device="cuda"), 1e-3)
+    bed.spectral_power(a.detach().clone().requires_grad_(True), -0.5).sum().backward()
+# full scatter CTAs, a chunked medium-path workspace, diagnostics outputs
+bed.scatter_matrices(torch.randn(200, 4, 9, device="cuda"), 0.0)
+a = torch.from_numpy(oracle.gen_spd(300, 20, 2).astype(np.float32)).cuda()
+cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=80)
+lam = torch.empty((300, 20), device="cuda")
+vec = torch.empty((300, 20, 20), device="cuda")
+bed.forward_into(a, cfg, lam, vec, ws=bed.workspace(a, cfg, max_bytes=1))
+bed.batched_eig(a, cfg)
 # chunked host path and a batch above the medium path's sub-warp tails
 x = oracle.gen_spd(3000, 4, 1).astype(np.float32)
 bed.batched_eig(x, bed.SolverConfig(deflation_tol=3e-12))
