@@ -56,6 +56,8 @@ def work_per_matrix(n: int, mode: str):
     b_fwd = 4 * (2 * n * n + n)
     if mode == "fwd":
         return f_fwd, b_fwd
+    if mode == "val":  # eigenvalues only (solver.py:94-109): no P, no fold
+        return (4.0 / 3.0) * n ** 3 + 24 * n * (n - 1), 4 * (n * n + n)
     if mode == "fwdpow":  # + spectral power V diag(f) V^T: one n^3 product
         return f_fwd + 2 * n ** 3, b_fwd + 4 * (2 * n * n + n)
     f_bwd = 6 * n ** 3 + 22 * n * n
@@ -142,7 +144,8 @@ class Step:
     def __init__(self, torch, bed, n, batch, mode, dev, seed):
         self.torch, self.bed, self.n, self.batch, self.mode = torch, bed, n, batch, mode
         self.a = make_inputs(torch, n, batch, mode, seed, dev)
-        self.cfg = bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n)
+        self.cfg = bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n,
+                                    compute_vectors=mode != "val")
         self.lam = torch.empty((batch, n), device=dev)
         self.vec = torch.empty((batch, n, n), device=dev)
         self.status = torch.empty((batch,), device=dev, dtype=torch.int32)
@@ -154,10 +157,12 @@ class Step:
             g = torch.Generator(device=dev).manual_seed(seed + 1)
             self.gv = torch.randn((batch, n, n), device=dev, generator=g)
             self.gl = torch.randn((batch, n), device=dev, generator=g)
-        self.launches = 1 if mode == "fwd" else 2
+        self.ws = bed.workspace(self.a, self.cfg)  # n >= 9: allocated once, outside the timed steps
+        self.launches = 1 if mode in ("fwd", "val") else 2
 
     def __call__(self):
-        self.bed.forward_into(self.a, self.cfg, self.lam, self.vec, self.status, self.steps)
+        self.bed.forward_into(self.a, self.cfg, self.lam, self.vec, self.status, self.steps,
+                              ws=self.ws)
         if self.mode == "fwdpow":  # A^(-1/2), the decorrelated-BN / ZCA consumer
             from paper_2207_04228_b200 import _native
 
@@ -410,7 +415,8 @@ def other_configs(torch, bed, dev, hbm_peak):
     cases = [(4, 512, "fwd"), (8, 512, "fwd"), (16, 512, "fwd"), (24, 512, "fwd"), (32, 512, "fwd"),
              (8, 1 << 20, "fwd"), (16, 1 << 18, "fwd"), (24, 1 << 17, "fwd"), (32, 1 << 16, "fwd"),
              (64, 8192, "fwd"), (16, 65536, "fwdbwd"), (64, 8192, "fwdbwd"),
-             (16, 65536, "fwdpow"), (64, 8192, "fwdpow")]
+             (16, 65536, "fwdpow"), (64, 8192, "fwdpow"),
+             (4, 1 << 22, "val"), (16, 1 << 18, "val"), (32, 1 << 16, "val"), (64, 8192, "val")]
     for n, b, mode in cases:
         st = Step(torch, bed, n, b, mode, dev, seed=n)
         reps = 50 if b <= 4096 else 10
