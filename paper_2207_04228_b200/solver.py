@@ -392,8 +392,10 @@ def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None
     ``zca_whiten``, solver.py:146-169): the unnormalised scatter
     (X - mu)(X - mu)^T + eps_reg I is decomposed on the GPU and its inverse
     square root (``matrix_power(-0.5, floor=0)``) applied to the centred
-    features.  The scatter and the final product are torch batched matmuls
-    (the covariance producer is SURVEY.md 8(f) row 3, not fused yet).
+    features.  The scatter is the native covariance producer
+    (``scatter_matrices`` / ``bed_scatter_f32``), the ED and the inverse
+    square root are the native kernels, and the final product
+    ``A^(-1/2) (X - mu)`` is a torch batched matmul.
     """
     if eps_reg < 0:
         raise ValueError("eps_reg must be nonnegative")
