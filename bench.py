@@ -60,6 +60,8 @@ def work_per_matrix(n: int, mode: str):
         return (4.0 / 3.0) * n ** 3 + 24 * n * (n - 1), 4 * (n * n + n)
     if mode == "fwdpow":  # + spectral power V diag(f) V^T: one n^3 product
         return f_fwd + 2 * n ** 3, b_fwd + 4 * (2 * n * n + n)
+    if mode == "powf":  # eigenvalues + A^p in one call: V never returned (bed_forward_power_f32)
+        return f_fwd + 2 * n ** 3, b_fwd
     f_bwd = 6 * n ** 3 + 22 * n * n
     b_bwd = 4 * (3 * n * n + 2 * n)
     return f_fwd + f_bwd, b_fwd + b_bwd
@@ -158,9 +160,25 @@ class Step:
             self.gv = torch.randn((batch, n, n), device=dev, generator=g)
             self.gl = torch.randn((batch, n), device=dev, generator=g)
         self.ws = bed.workspace(self.a, self.cfg)  # n >= 9: allocated once, outside the timed steps
-        self.launches = 1 if mode in ("fwd", "val") else 2
+        if mode == "powf":
+            from paper_2207_04228_b200 import _native
+
+            self.pws_bytes = _native.power_workspace_bytes(batch, n, _native.make_config(self.cfg, n))
+            self.pws = torch.empty((self.pws_bytes + 256,), dtype=torch.uint8, device=dev)
+            self.pws_ptr = (self.pws.data_ptr() + 255) & ~255 if self.pws_bytes else None
+            self.steps.zero_()
+        self.launches = 1 if mode in ("fwd", "val") or (mode == "powf" and n <= 8) else 2
 
     def __call__(self):
+        if self.mode == "powf":
+            from paper_2207_04228_b200 import _native
+
+            c = _native.make_config(self.cfg, self.n)
+            _native.forward_power_f32(self.a.data_ptr(), self.batch, self.n, self.lam.data_ptr(),
+                                      self.vec.data_ptr(), self.status.data_ptr(), None, c, -0.5, -1.0,
+                                      self.pws_ptr, self.pws_bytes,
+                                      self.torch.cuda.current_stream().cuda_stream)
+            return
         self.bed.forward_into(self.a, self.cfg, self.lam, self.vec, self.status, self.steps,
                               ws=self.ws)
         if self.mode == "fwdpow":  # A^(-1/2), the decorrelated-BN / ZCA consumer
@@ -416,7 +434,8 @@ def other_configs(torch, bed, dev, hbm_peak):
              (8, 1 << 20, "fwd"), (16, 1 << 18, "fwd"), (24, 1 << 17, "fwd"), (32, 1 << 16, "fwd"),
              (64, 8192, "fwd"), (16, 65536, "fwdbwd"), (64, 8192, "fwdbwd"),
              (16, 65536, "fwdpow"), (64, 8192, "fwdpow"),
-             (4, 1 << 22, "val"), (16, 1 << 18, "val"), (32, 1 << 16, "val"), (64, 8192, "val")]
+             (4, 1 << 22, "val"), (16, 1 << 18, "val"), (32, 1 << 16, "val"), (64, 8192, "val"),
+             (4, 1 << 22, "fwdpow"), (4, 1 << 22, "powf"), (16, 65536, "powf")]
     for n, b, mode in cases:
         st = Step(torch, bed, n, b, mode, dev, seed=n)
         reps = 50 if b <= 4096 else 10
@@ -430,7 +449,7 @@ def other_configs(torch, bed, dev, hbm_peak):
                "roofline_bound": bound, "roofline_frac": frac,
                "mean_double_steps": float(stp.mean()),
                # warp-synchronous QR: lanes idle once their matrix is done
-               "qr_useful_lane_frac": float(stp.mean() / wmax)}
+               "qr_useful_lane_frac": float(stp.mean() / wmax) if float(wmax) > 0 else None}
         if mode == "fwd":
             te = torch_eigh_ms(torch, st.a)
             row["torch_eigh_ms"] = te

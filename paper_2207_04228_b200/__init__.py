@@ -30,6 +30,7 @@ from .solver import (  # noqa: F401
     eigh,
     forward_into,
     matrix_power,
+    power_of,
     scatter_matrices,
     spectral_power,
     SpectralPowerFn,

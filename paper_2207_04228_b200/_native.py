@@ -28,6 +28,8 @@ EXPORTS = (
     "bed_forward_host_f32",
     "bed_backward_f32",
     "bed_matrix_power_f32",
+    "bed_forward_power_f32",
+    "bed_forward_power_workspace_bytes",
     "bed_scatter_f32",
     "bed_error_string",
     "bed_last_cuda_error",
@@ -82,6 +84,11 @@ def lib() -> ctypes.CDLL:
     L.bed_matrix_power_f32.restype = ctypes.c_int
     L.bed_matrix_power_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, ctypes.c_float,
                                        ctypes.c_float, vp]
+    L.bed_forward_power_f32.restype = ctypes.c_int
+    L.bed_forward_power_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, ctypes.POINTER(BedConfig),
+                                        ctypes.c_float, ctypes.c_float, vp, ctypes.c_size_t, vp]
+    L.bed_forward_power_workspace_bytes.restype = ctypes.c_size_t
+    L.bed_forward_power_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(BedConfig)]
     L.bed_scatter_f32.restype = ctypes.c_int
     L.bed_scatter_f32.argtypes = [vp, i64, i32, i32, ctypes.c_float, vp, vp]
     L.bed_error_string.restype = ctypes.c_char_p
@@ -152,6 +159,17 @@ def matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n,
     rc = lib().bed_matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n,
                                     p, floor, stream)
     check(rc, "bed_matrix_power_f32")
+
+
+def forward_power_f32(A_ptr, batch, n, evals_ptr, out_ptr, status_ptr, flags_ptr, cfg: BedConfig,
+                      p, floor, ws_ptr, ws_bytes, stream) -> None:
+    rc = lib().bed_forward_power_f32(A_ptr, batch, n, evals_ptr, out_ptr, status_ptr, flags_ptr,
+                                     ctypes.byref(cfg), p, floor, ws_ptr, ws_bytes, stream)
+    check(rc, "bed_forward_power_f32")
+
+
+def power_workspace_bytes(batch: int, n: int, cfg: BedConfig) -> int:
+    return int(lib().bed_forward_power_workspace_bytes(batch, n, ctypes.byref(cfg)))
 
 
 def scatter_f32(X_ptr, batch, n, m, eps, out_ptr, stream) -> None:

@@ -207,6 +207,52 @@ int bed_forward_f32(const float* A, int64_t batch, int32_t n, float* evals, floa
   return rc;
 }
 
+size_t bed_forward_power_workspace_bytes(int64_t batch, int32_t n, const bed_config* cfg) {
+  if (!cfg || batch <= 0 || n <= 8 || n > 64) return 0;
+  bed_config c = *cfg;
+  c.compute_vectors = 1;
+  return align_up(sizeof(float) * (size_t)batch * n * n) + bed_forward_workspace_bytes(batch, n, &c);
+}
+
+int bed_forward_power_f32(const float* A, int64_t batch, int32_t n, float* evals, float* out,
+                          int32_t* status, int32_t* flags, const bed_config* cfg, float p,
+                          float floor, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!cfg || !(p == p)) return BED_ERR_INVALID_ARGUMENT;
+  bed_config cv = *cfg;
+  cv.compute_vectors = 1;
+  int rc = check_forward(A, batch, n, evals, out, &cv);
+  if (rc) return rc;
+  if (!aligned4(status) || !aligned4(flags) || (reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return BED_ERR_MISALIGNED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags) {
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "bed_forward_power_f32 memset(flags)");
+  }
+  if (batch == 0) return BED_SUCCESS;
+  const int needs_positive = (p < 0.0f || p != floorf(p)) ? 1 : 0;  // solver.py:133
+  if (n <= 8) {  // fused: V stays in the thread that formed it
+    const bed::PowSpec spec{p, floor, needs_positive};
+    bed::FwdArgs a{A, batch, n, evals, out, status, nullptr, flags, kernel_cfg(&cv, n), s,
+                   bed::DiagOut{nullptr, nullptr}, nullptr, 0, &spec};
+    cudaError_t e = bed::launch_small(a);
+    if (e != cudaSuccess) return cuda_fail(e, "bed_forward_power_f32 launch");
+    return BED_SUCCESS;
+  }
+  const size_t vbytes = align_up(sizeof(float) * (size_t)batch * n * n);
+  if (!workspace || workspace_bytes < vbytes) return BED_ERR_INVALID_ARGUMENT;
+  float* V = static_cast<float*>(workspace);
+  // the forward's statuses and flags, then the power ORs in NonPositiveSpectrum
+  rc = bed_forward_ws_f32(A, batch, n, evals, V, status, nullptr, flags, nullptr, nullptr, &cv,
+                          static_cast<char*>(workspace) + vbytes, workspace_bytes - vbytes, stream);
+  if (rc) return rc;
+  bed::PowArgs pa{V, evals, out, status, flags, batch, n, p, floor, needs_positive, s};
+  pa.merge = 1;
+  cudaError_t e = bed::launch_power(pa);
+  if (e != cudaSuccess) return cuda_fail(e, "bed_forward_power_f32 power launch");
+  return BED_SUCCESS;
+}
+
 int bed_backward_f32(const float* V, const float* evals, const float* gV, const float* gL,
                      float* gA, int64_t batch, int32_t n, int32_t taylor_degree, int32_t* status,
                      int32_t* flags, void* stream) {

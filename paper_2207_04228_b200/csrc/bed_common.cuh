@@ -52,6 +52,26 @@ struct DiagOut {
   }
 };
 
+// f(x) = x^p of the spectral power (matrix_power, solver.py:115-143), exact
+// for the common powers.
+__device__ __forceinline__ float spectral_pow(float x, float p) {
+  if (p == 1.0f) return x;
+  if (p == 2.0f) return x * x;
+  if (p == 0.5f) return sqrtf(x);
+  if (p == -0.5f) return 1.0f / sqrtf(x);
+  if (p == -1.0f) return 1.0f / x;
+  return powf(x, p);
+}
+
+// Spectral power fused into the forward (bed_forward_power_f32): out =
+// V diag(max(lambda, floor)^p) V^T instead of V.  floor_abs < 0 selects the
+// reference default 1e-12 * lambda_max per matrix (solver.py:131-132).
+struct PowSpec {
+  float p;
+  float floor_abs;
+  int needs_positive;  // p negative or fractional: a non-positive clamped eigenvalue is an error
+};
+
 struct KernelCfg {
   float eps;       // deflation_tol
   float sym_tol;   // symmetry_tol

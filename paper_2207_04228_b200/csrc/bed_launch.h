@@ -23,6 +23,7 @@ struct FwdArgs {
   DiagOut dg;       // optional per-matrix diagnostics
   void* ws;         // n >= 9: device workspace (bed_forward_workspace_bytes)
   size_t ws_bytes;  // a smaller workspace solves the batch in chunks
+  const PowSpec* pw = nullptr;  // n <= 8: write the spectral power to evecs instead of V
 };
 
 // Workspace bytes the n >= 9 path needs for `batch` matrices in one chunk
@@ -56,6 +57,7 @@ struct PowArgs {
   float floor_abs;  // < 0: 1e-12 * lambda_max per matrix
   int needs_positive;
   cudaStream_t stream;
+  int merge = 0;    // 1: write status only for a non-positive spectrum (after a forward)
 };
 
 struct ScatArgs {

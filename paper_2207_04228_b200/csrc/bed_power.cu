@@ -30,21 +30,12 @@ struct PowParams {
   static constexpr size_t BYTES = sizeof(float) * (size_t)MB * PER;
 };
 
-__device__ __forceinline__ float spectral_pow(float x, float p) {
-  if (p == 1.0f) return x;
-  if (p == 2.0f) return x * x;
-  if (p == 0.5f) return sqrtf(x);
-  if (p == -0.5f) return 1.0f / sqrtf(x);
-  if (p == -1.0f) return 1.0f / x;
-  return powf(x, p);
-}
-
 template <int NMAX, bool EXACT>
 __global__ void __launch_bounds__(PowParams<NMAX>::THREADS)
     bed_power_kernel(const float* __restrict__ V, const float* __restrict__ lam,
                      float* __restrict__ out, int32_t* __restrict__ status,
                      int32_t* __restrict__ flags, int64_t batch, int n_rt, float p, float floor_abs,
-                     int needs_positive) {
+                     int needs_positive, int merge) {
   using P = PowParams<NMAX>;
   constexpr int SROW = P::SROW, TQ = P::TQ;
   const int n = EXACT ? NMAX : n_rt;
@@ -80,8 +71,12 @@ __global__ void __launch_bounds__(PowParams<NMAX>::THREADS)
       sf[c] = x;
     }
     for (int c = 0; c < n; ++c) sf[c] = bad ? 0.0f : spectral_pow(sf[c], p);
-    if (status) status[base + mi] = bad ? kStatusNonPositive : kStatusOk;
-    if (bad && flags) atomicOr(flags, 1 << kStatusNonPositive);
+    // merge (after a forward): a matrix the forward flagged keeps its status;
+    // an accepted one is flagged only for a non-positive spectrum
+    bool flag = bad;
+    if (merge) flag = bad && (!status || status[base + mi] == kStatusOk);
+    if (status && (flag || !merge)) status[base + mi] = flag ? kStatusNonPositive : kStatusOk;
+    if (flag && flags) atomicOr(flags, 1 << kStatusNonPositive);
   }
   __syncthreads();
   // V^T and diag(f) V^T from V
@@ -120,7 +115,7 @@ static cudaError_t go_pow(const PowArgs& a) {
   if (cudaError_t e = ensure_smem(kern, P::BYTES); e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.batch + P::MB - 1) / P::MB);
   kern<<<grid, P::THREADS, P::BYTES, a.stream>>>(a.V, a.lam, a.out, a.status, a.flags, a.batch,
-                                                 a.n, a.p, a.floor_abs, a.needs_positive);
+                                                 a.n, a.p, a.floor_abs, a.needs_positive, a.merge);
   return cudaGetLastError();
 }
 

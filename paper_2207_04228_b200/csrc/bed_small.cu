@@ -7,7 +7,10 @@ namespace bed {
 template <int N>
 static cudaError_t go_small(const FwdArgs& a) {
   const unsigned grid = (unsigned)((a.batch + kSmallThreads - 1) / kSmallThreads);
-  if (a.evecs)
+  if (a.pw)
+    bed_small_kernel<N, true, true><<<grid, kSmallThreads, 0, a.stream>>>(
+        a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg, *a.pw);
+  else if (a.evecs)
     bed_small_kernel<N, true><<<grid, kSmallThreads, 0, a.stream>>>(
         a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg);
   else

@@ -210,12 +210,17 @@ __device__ __forceinline__ int small_deflate_zero(float (&e)[N], int m, float ep
   return m;
 }
 
-template <int N, bool VECS>
+// POW: the spectral power V diag(max(lambda, floor)^p) V^T (matrix_power,
+// solver.py:115-143) is formed from V in registers and written to `evecs` in
+// place of V -- the fused epilogue of SURVEY.md 8(f) row 1; V never leaves
+// the thread.
+template <int N, bool VECS, bool POW = false>
 __global__ void __launch_bounds__(kSmallThreads)
     bed_small_kernel(const float* __restrict__ A, int64_t batch, float* __restrict__ evals,
                      float* __restrict__ evecs, int32_t* __restrict__ status_out,
                      int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg,
-                     DiagOut dg) {
+                     DiagOut dg, PowSpec pw = PowSpec{}) {
+  static_assert(!POW || VECS, "the power is formed from the eigenvectors");
   using Lay = SmallLayout<N>;
   constexpr int NN = Lay::NN;
   constexpr int NP = Lay::NP;
@@ -504,7 +509,35 @@ __global__ void __launch_bounds__(kSmallThreads)
     float* lrow = ltile + tid * Lay::LSTRIDE;
 #pragma unroll
     for (int c = 0; c < N; ++c) lrow[rank[c]] = d[c] * scale;
-    if constexpr (VECS) {
+    if constexpr (POW) {
+      // f_k = max(lambda_k, floor)^p with the per-matrix floor (solver.py:127-139)
+      float lmax = d[0] * scale;
+#pragma unroll
+      for (int k = 1; k < N; ++k) lmax = fmaxf(lmax, d[k] * scale);
+      const float fl = pw.floor_abs < 0.0f ? 1e-12f * lmax : pw.floor_abs;
+      float f[N];
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const float x = fmaxf(d[k] * scale, fl);
+        bad = bad || (pw.needs_positive && !(x > 0.0f));
+        f[k] = x;
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) f[k] = bad ? 0.0f : spectral_pow(f[k], pw.p);
+      if (bad && status == kStatusOk) status = kStatusNonPositive;
+      float* my = tile + tid * Lay::STRIDE;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = r; c < N; ++c) {  // symmetric by construction (solver.py:141)
+          float acc = 0.0f;
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc = fmaf(v_at<NP, N>(v, r, k) * f[k], v_at<NP, N>(v, c, k), acc);
+          my[r * N + c] = acc;
+          my[c * N + r] = acc;
+        }
+    } else if constexpr (VECS) {
       float* my = tile + tid * Lay::STRIDE;
 #pragma unroll
       for (int c = 0; c < N; ++c) {

@@ -30,7 +30,7 @@ from .core import (
 )
 
 __all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into", "workspace",
-           "spectral_power", "SpectralPowerFn",
+           "spectral_power", "SpectralPowerFn", "power_of",
            "matrix_power", "zca_whiten", "scatter_matrices", "TAYLOR_DEGREE"]
 
 TAYLOR_DEGREE = 9
@@ -350,6 +350,8 @@ class SpectralPowerFn(torch.autograd.Function):
     def forward(ctx, A, p: float, cfg: SolverConfig | None = None, floor: float | None = None,
                 degree: int = TAYLOR_DEGREE, check: bool = True):
         cfg = cfg or SolverConfig()
+        if not ctx.needs_input_grad[0]:  # inference: V is not needed afterwards
+            return power_of(A.detach(), p, cfg, floor, check)
         evals, evecs, _, _, _ = _solve_device(A.detach(), cfg, check=check)
         out = _power_device(evecs, evals, p, floor) if check else _power_nocheck(evecs, evals, p, floor)
         ctx.save_for_backward(evals, evecs)
@@ -376,6 +378,37 @@ def _power_nocheck(V, lam, p, floor):
     with torch.cuda.device(V.device):
         _native.matrix_power_f32(V.data_ptr(), lam.data_ptr(), out.data_ptr(), None, None, b, n, float(p),
                                  -1.0 if floor is None else float(floor), _stream_handle(V.device))
+    return out
+
+
+def power_of(A: torch.Tensor, p: float, cfg: SolverConfig | None = None,
+             floor: float | None = None, check: bool = True) -> torch.Tensor:
+    """V diag(max(lambda, floor)^p) V^T of a CUDA float32 batch in one call
+    (C ABI ``bed_forward_power_f32``): for n <= 8 the power is formed in the
+    forward kernel's epilogue and V never reaches memory.  Raises like
+    ``batched_eig`` and ``matrix_power`` when ``check``."""
+    cfg = cfg or SolverConfig()
+    A = _check_cuda_f32(A, "A")
+    b, n, _ = A.shape
+    c = _native.make_config(cfg, n)
+    out = torch.empty_like(A)
+    evals = torch.empty((b, n), device=A.device, dtype=torch.float32)
+    status = torch.empty((b,), device=A.device, dtype=torch.int32)
+    flags = torch.empty((1,), device=A.device, dtype=torch.int32)
+    wb = _native.power_workspace_bytes(b, n, c)
+    ws = torch.empty((wb + 256,), dtype=torch.uint8, device=A.device) if wb else None
+    wp = ((ws.data_ptr() + 255) & ~255) if ws is not None else None
+    with torch.cuda.device(A.device):
+        _native.forward_power_f32(A.data_ptr(), b, n, evals.data_ptr(), out.data_ptr(),
+                                  status.data_ptr(), flags.data_ptr(), c, float(p),
+                                  -1.0 if floor is None else float(floor), wp, wb,
+                                  _stream_handle(A.device))
+    if check:
+        fl = int(flags.item())
+        _raise_for_status(A, status, fl & ~(1 << _native.STATUS_NON_POSITIVE), cfg)
+        if fl & (1 << _native.STATUS_NON_POSITIVE):
+            k = int(torch.nonzero(status == _native.STATUS_NON_POSITIVE)[0, 0])
+            raise NonPositiveSpectrum(k, float(evals[k].min()))
     return out
 
 

@@ -235,3 +235,41 @@ def test_spectral_power_gradient_matches_oracle_chain(bed, n):
     gl = np.diagonal(v.transpose(0, 2, 1) @ g @ v, axis1=1, axis2=2) * df
     ref = oracle.taylor_backward(v, lam, gv, gl)
     assert P.grad_err(at.grad.cpu().numpy(), ref).max() <= 1e-4
+
+
+# ---- eigenvalues + spectral power in one call (bed_forward_power_f32; fused for n <= 8)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 9, 16, 24, 40])
+@pytest.mark.parametrize("p", [-0.5, 0.5, 2.0, -1.0, 0.3])
+def test_power_of_matches_two_step_path(bed, n, p):
+    a = torch.from_numpy(_cov(300, n, 4 * n, 300 + n)).cuda()
+    cfg = bed.SolverConfig(deflation_tol=3e-12)
+    got = bed.power_of(a, p, cfg).cpu().numpy().astype(np.float64)
+    e = bed.batched_eig(a, cfg)
+    ref, bad = oracle.matrix_power(e.eigenvectors.cpu().numpy(), e.eigenvalues.cpu().numpy(), p)
+    assert not bad.any()
+    err = np.linalg.norm(got - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
+    assert err.max() <= 1e-5, err.max()
+    np.testing.assert_array_equal(got, got.transpose(0, 2, 1))
+
+
+@pytest.mark.parametrize("n", [4, 16])
+def test_power_of_errors_and_default_floor(bed, n):
+    a = np.stack([np.eye(n, dtype=np.float32)] * 5)
+    a[3] *= -1.0  # negative spectrum
+    at = torch.from_numpy(a).cuda()
+    with pytest.raises(bed.NonPositiveSpectrum) as err:
+        bed.power_of(at, -0.5, floor=0.0)
+    assert err.value.batch_index == 3
+    sq = bed.power_of(at, 2.0, floor=0.0).cpu().numpy()  # integer power: no check
+    np.testing.assert_allclose(sq[3], np.zeros((n, n)), atol=0)  # max(-1, 0)^2
+    bad = a.copy()
+    bad[1, 0, 1] = np.nan
+    with pytest.raises(bed.NonFinite):
+        bed.power_of(torch.from_numpy(bad).cuda(), 0.5)
+    # the differentiable entry takes the fused path when no gradient is needed
+    x = torch.from_numpy(_cov(64, n, 4 * n, 5)).cuda()
+    with torch.no_grad():
+        y = bed.spectral_power(x, -0.5)
+    np.testing.assert_allclose(y.cpu().numpy(), bed.power_of(x, -0.5).cpu().numpy(), rtol=0, atol=0)
