@@ -36,8 +36,8 @@
  *                          way the reference API is called (solver.py:79)
  *   bed_backward_f32       (absent in the reference: pkg/README.md:116-117)
  *                          ED backward with Taylor-K
- *   bed_forward_power_f32  batched_eig() + matrix_power() in one call, V not returned
- *                          (fused into the forward's epilogue for n <= 8)
+ *   bed_forward_power_f32  batched_eig() + matrix_power() in one call, fused into the
+ *                          forward's epilogue for n <= 24 (V never written)
  *   bed_matrix_power_f32   matrix_power()           solver.py:115-143
  *                          (the ED's spectral-
  *                          function consumer, V diag(f(lambda)) V^T)
@@ -165,9 +165,11 @@ int bed_matrix_power_f32(const float* V, const float* evals, float* out, int32_t
 
 /* Eigenvalues and the spectral power  out = V diag(max(evals, floor)^p) V^T  in one
  * call (reference batched_eig + matrix_power, solver.py:79-143),
- * without returning V.  n <= 8: fused -- the power is formed from V in the registers
- * of the thread that solved the matrix, V never reaches memory; n >= 9: V goes to the
- * workspace (bed_forward_power_workspace_bytes) and the power kernel reads it.
+ * without returning V.  n <= 24: the power is formed in the forward's epilogue (n <= 8:
+ * from V in the registers of the thread that solved the matrix; 9 <= n <= 24: in the
+ * eigenvector fold, from V in registers and shared memory), so V never reaches memory;
+ * n >= 25: V goes to the workspace and the tiled power kernel reads it.  Workspace:
+ * bed_forward_power_workspace_bytes.
  * cfg->compute_vectors is ignored (vectors are implied); floor < 0 = the reference
  * default 1e-12 * max(evals); status/flags as bed_forward_f32, plus
  * BED_STATUS_NON_POSITIVE as bed_matrix_power_f32.  out is symmetric. */

@@ -89,10 +89,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-template <int NMAX, bool EXACT>
+// POW: instead of V, write the spectral power V diag(max(lambda, floor)^p) V^T
+// (matrix_power, solver.py:115-143) to `evecs` -- formed from V in registers
+// and a shared copy of it, so V never reaches memory.
+// Each entry sums fma(V[r][k] V[c][k], f_k) in k order, which is symmetric in
+// (r, c), so the output is exactly symmetric (solver.py:141).
+template <int NMAX, bool EXACT, bool POW = false>
 __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
     bed_fold_tma_kernel(int64_t bc, int64_t c0, int n_rt, SplitWs ws, float* __restrict__ evals,
-                        float* __restrict__ evecs, KernelCfg cfg) {
+                        float* __restrict__ evecs, KernelCfg cfg, PowSpec pw = PowSpec{},
+                        int32_t* __restrict__ status_out = nullptr, int32_t* __restrict__ flags = nullptr) {
   using P = FTParams<NMAX>;
   constexpr int LF = P::LF, R = P::R, RP = P::RP, MPC = P::MPC, NB = P::NB, POS = P::POS;
   const int n = EXACT ? NMAX : n_rt;
@@ -275,7 +281,55 @@ __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
     }
   }
   __syncthreads();
-  if (mlive) {
+  if constexpr (POW) {
+    static_assert(R % 2 == 0, "power epilogue on packed row pairs");
+    float* fv = flipv;  // f_k per matrix, unsorted order (as V's columns)
+    if (mlive) {
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+        const int r0 = l + LF * (2 * rp), r1 = r0 + LF;
+#pragma unroll
+        for (int c = 0; c < NMAX; ++c) {
+          if (r0 < NMAX) st[r0 * P::SROW + c] = f2_lo(v[rp][c]);
+          if (r1 < NMAX) st[r1 * P::SROW + c] = f2_hi(v[rp][c]);
+        }
+      }
+      if (l == 0) {  // floor, positivity check, f (solver.py:127-139)
+        float lmax = lams[mi * NMAX];
+        for (int k = 1; k < n; ++k) lmax = fmaxf(lmax, lams[mi * NMAX + k]);
+        const float fl = pw.floor_abs < 0.0f ? 1e-12f * lmax : pw.floor_abs;
+        bool bad = false;
+        for (int k = 0; k < n; ++k) {
+          const float x = fmaxf(lams[mi * NMAX + k], fl);
+          bad = bad || (pw.needs_positive && !(x > 0.0f));
+          fv[mi * NMAX + k] = x;
+        }
+        for (int k = 0; k < NMAX; ++k) fv[mi * NMAX + k] = (bad || k >= n) ? 0.0f : spectral_pow(fv[mi * NMAX + k], pw.p);
+        const int64_t j = c0 + j0 + mi;
+        if (bad && (!status_out || status_out[j] == kStatusOk)) {  // the forward's status wins
+          if (status_out) status_out[j] = kStatusNonPositive;
+          if (flags) atomicOr(flags, 1 << kStatusNonPositive);
+        }
+      }
+    }
+    __syncthreads();
+    if (mlive) {
+      const float* fk = fv + mi * NMAX;
+      float* om = evecs + (c0 + j0 + mi) * nn;
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+        const int r0 = l + LF * (2 * rp), r1 = r0 + LF;
+        for (int c = 0; c < n; ++c) {
+          const float* vc = st + c * P::SROW;
+          f2 acc = f2_bc(0.0f);
+#pragma unroll
+          for (int k = 0; k < NMAX; ++k) acc = ffma2(fmul2(v[rp][k], f2_bc(vc[k])), f2_bc(fk[k]), acc);
+          if (r0 < n) om[r0 * n + c] = f2_lo(acc);
+          if (r1 < n) om[r1 * n + c] = f2_hi(acc);
+        }
+      }
+    }
+  } else if (mlive) {
     if constexpr (R == 1) {
 #pragma unroll
       for (int c = 0; c < NMAX; ++c)
@@ -295,6 +349,7 @@ __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
       }
     }
   }
+  if constexpr (!POW) {
   __syncthreads();
   if (mlive) {  // sign: the largest-magnitude entry of each column is >= 0
 #pragma unroll
@@ -315,6 +370,7 @@ __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
   }
   __syncthreads();
   stage_to_tile<NMAX, P::THREADS, P::SROW, P::SMAT>(smem, count, n, evecs + (c0 + j0) * nn, flipv);
+  }
   float* dstl = evals + (c0 + j0) * n;
   for (int g = tid; g < count * n; g += P::THREADS) {
     const int mat = g / n, c = g - mat * n;

@@ -46,8 +46,13 @@ cudaError_t launch_qf(const FwdArgs& a, const SplitWs& ws, int64_t c0, int64_t b
     using FP = FTParams<NMAX>;
     bed_qr_kernel<NMAX, EXACT, true><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0, st>>>(
         bc, c0, n, ws, a.evals, a.status, a.steps, a.flags, a.cfg, a.dg);
-    bed_fold_tma_kernel<NMAX, EXACT><<<(unsigned)((bc + FP::MPC - 1) / FP::MPC), FP::THREADS, FP::BYTES,
-                                       st>>>(bc, c0, n, ws, a.evals, a.evecs, a.cfg);
+    if (a.pw)  // spectral power in the fold's epilogue (V never reaches memory)
+      bed_fold_tma_kernel<NMAX, EXACT, true><<<(unsigned)((bc + FP::MPC - 1) / FP::MPC), FP::THREADS,
+                                               FP::BYTES, st>>>(bc, c0, n, ws, a.evals, a.evecs, a.cfg,
+                                                                *a.pw, a.status, a.flags);
+    else
+      bed_fold_tma_kernel<NMAX, EXACT><<<(unsigned)((bc + FP::MPC - 1) / FP::MPC), FP::THREADS, FP::BYTES,
+                                         st>>>(bc, c0, n, ws, a.evals, a.evecs, a.cfg);
   } else {
     bed_qr_kernel<NMAX, EXACT, false><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0, st>>>(
         bc, c0, n, ws, a.evals, a.status, a.steps, a.flags, a.cfg, a.dg);
@@ -64,6 +69,7 @@ cudaError_t run_split(const FwdArgs& a) {
   cudaError_t e = ensure_smem(vecs ? bed_hh_kernel<NMAX, EXACT, true> : bed_hh_kernel<NMAX, EXACT, false>,
                               HP::BYTES);
   if (e == cudaSuccess && vecs) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT>, FTParams<NMAX>::BYTES);
+  if (e == cudaSuccess && a.pw) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT, true>, FTParams<NMAX>::BYTES);
   if (e != cudaSuccess) return e;
   char* base = static_cast<char*>(a.ws);
 
