@@ -43,6 +43,8 @@
  *                          function consumer, V diag(f(lambda)) V^T)
  *   bed_scatter_f32        the scatter inside zca_whiten()  solver.py:161-166
  *                          (covariance producer)
+ *   bed_scatter_forward_f32  scatter + batched_eig [+ matrix_power]  solver.py:79-166,
+ *                          one kernel for n <= 8 (the covariance never written)
  *   bed_error_string       error text for the integer return codes; the
  *                          reference maps kernel status ints to exceptions
  *                          in qr.py:604-609 / oracle.py:76-79
@@ -184,6 +186,22 @@ int bed_forward_power_f32(const float* A, int64_t batch, int32_t n, float* evals
  * out (batch, n, n).  Device pointers, stream-ordered. */
 int bed_scatter_f32(const float* X, int64_t batch, int32_t n, int32_t m, float eps, float* out,
                     void* stream);
+
+/* Covariance -> eigendecomposition in one call (SURVEY.md 8(f) row 3 feeding row 1;
+ * reference zca_whiten's scatter + batched_eig [+ matrix_power], solver.py:79-166):
+ * A = sym((X - mu)(X - mu)^T) + eps I formed from X (batch, n, m) as bed_scatter_f32
+ * does, then solved as bed_forward_f32 (power == 0: out = V when cfg->compute_vectors,
+ * else unused) or bed_forward_power_f32 (power != 0: out = A^p with floor as there).
+ * n <= 8: ONE kernel -- each thread forms its matrix from X in registers, so A never
+ * reaches memory and no workspace is needed; n >= 9: A goes to the workspace, sized by
+ * bed_scatter_forward_workspace_bytes.  status/flags as bed_forward_f32 /
+ * bed_forward_power_f32; a non-finite sample in X gives BED_STATUS_NON_FINITE. */
+size_t bed_scatter_forward_workspace_bytes(int64_t batch, int32_t n, int32_t m,
+                                           const bed_config* cfg, int32_t power);
+int bed_scatter_forward_f32(const float* X, int64_t batch, int32_t n, int32_t m, float eps,
+                            float* evals, float* out, int32_t* status, int32_t* flags,
+                            const bed_config* cfg, int32_t power, float p, float floor,
+                            void* workspace, size_t workspace_bytes, void* stream);
 
 const char* bed_error_string(int code);
 const char* bed_last_cuda_error(void); /* thread-local text of the last BED_ERR_CUDA */

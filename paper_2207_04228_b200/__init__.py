@@ -32,6 +32,8 @@ from .solver import (  # noqa: F401
     matrix_power,
     power_of,
     scatter_matrices,
+    scatter_eig,
+    scatter_power,
     spectral_power,
     SpectralPowerFn,
     taylor_backward,

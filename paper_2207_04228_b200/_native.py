@@ -31,6 +31,8 @@ EXPORTS = (
     "bed_forward_power_f32",
     "bed_forward_power_workspace_bytes",
     "bed_scatter_f32",
+    "bed_scatter_forward_f32",
+    "bed_scatter_forward_workspace_bytes",
     "bed_error_string",
     "bed_last_cuda_error",
     "bed_abi_version",
@@ -91,6 +93,12 @@ def lib() -> ctypes.CDLL:
     L.bed_forward_power_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(BedConfig)]
     L.bed_scatter_f32.restype = ctypes.c_int
     L.bed_scatter_f32.argtypes = [vp, i64, i32, i32, ctypes.c_float, vp, vp]
+    L.bed_scatter_forward_f32.restype = ctypes.c_int
+    L.bed_scatter_forward_f32.argtypes = [vp, i64, i32, i32, ctypes.c_float, vp, vp, vp, vp,
+                                          ctypes.POINTER(BedConfig), i32, ctypes.c_float,
+                                          ctypes.c_float, vp, ctypes.c_size_t, vp]
+    L.bed_scatter_forward_workspace_bytes.restype = ctypes.c_size_t
+    L.bed_scatter_forward_workspace_bytes.argtypes = [i64, i32, i32, ctypes.POINTER(BedConfig), i32]
     L.bed_error_string.restype = ctypes.c_char_p
     L.bed_error_string.argtypes = [ctypes.c_int]
     L.bed_last_cuda_error.restype = ctypes.c_char_p
@@ -170,6 +178,18 @@ def forward_power_f32(A_ptr, batch, n, evals_ptr, out_ptr, status_ptr, flags_ptr
 
 def power_workspace_bytes(batch: int, n: int, cfg: BedConfig) -> int:
     return int(lib().bed_forward_power_workspace_bytes(batch, n, ctypes.byref(cfg)))
+
+
+def scatter_forward_f32(X_ptr, batch, n, m, eps, evals_ptr, out_ptr, status_ptr, flags_ptr,
+                        cfg: BedConfig, power, p, floor, ws_ptr, ws_bytes, stream) -> None:
+    rc = lib().bed_scatter_forward_f32(X_ptr, batch, n, m, eps, evals_ptr, out_ptr, status_ptr,
+                                       flags_ptr, ctypes.byref(cfg), int(power), p, floor, ws_ptr,
+                                       ws_bytes, stream)
+    check(rc, "bed_scatter_forward_f32")
+
+
+def scatter_forward_workspace_bytes(batch: int, n: int, m: int, cfg: BedConfig, power) -> int:
+    return int(lib().bed_scatter_forward_workspace_bytes(batch, n, m, ctypes.byref(cfg), int(power)))
 
 
 def scatter_f32(X_ptr, batch, n, m, eps, out_ptr, stream) -> None:

@@ -316,6 +316,60 @@ int bed_scatter_f32(const float* X, int64_t batch, int32_t n, int32_t m, float e
   return BED_SUCCESS;
 }
 
+size_t bed_scatter_forward_workspace_bytes(int64_t batch, int32_t n, int32_t m,
+                                           const bed_config* cfg, int32_t power) {
+  if (!cfg || batch <= 0 || n <= 8 || n > 64 || m < 1) return 0;
+  return align_up(sizeof(float) * (size_t)batch * n * n) +
+         (power ? bed_forward_power_workspace_bytes(batch, n, cfg)
+                : bed_forward_workspace_bytes(batch, n, cfg));
+}
+
+int bed_scatter_forward_f32(const float* X, int64_t batch, int32_t n, int32_t m, float eps,
+                            float* evals, float* out, int32_t* status, int32_t* flags,
+                            const bed_config* cfg, int32_t power, float p, float floor,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  if (m < 1 || !(eps >= 0.0f) || (power && !(p == p))) return BED_ERR_INVALID_ARGUMENT;
+  if (!cfg) return BED_ERR_INVALID_ARGUMENT;
+  bed_config cv = *cfg;
+  if (power) cv.compute_vectors = 1;
+  int rc = check_forward(X, batch, n, evals, out, &cv);
+  if (rc) return rc;
+  if (!aligned4(status) || !aligned4(flags) || (reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return BED_ERR_MISALIGNED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n > 8) {  // composed: the scatter kernel writes S to the workspace, the forward reads it
+    const size_t sbytes = align_up(sizeof(float) * (size_t)batch * n * n);
+    if (batch > 0 && (!workspace || workspace_bytes < sbytes)) return BED_ERR_INVALID_ARGUMENT;
+    float* S = static_cast<float*>(workspace);
+    if (batch > 0) {
+      bed::ScatArgs sa{X, S, batch, n, m, eps, s};
+      cudaError_t e = bed::launch_scatter(sa);
+      if (e != cudaSuccess) return cuda_fail(e, "bed_scatter_forward_f32 scatter launch");
+    }
+    void* rest = batch > 0 ? static_cast<char*>(workspace) + sbytes : workspace;
+    const size_t rest_bytes = batch > 0 ? workspace_bytes - sbytes : workspace_bytes;
+    return power ? bed_forward_power_f32(S, batch, n, evals, out, status, flags, &cv, p, floor, rest,
+                                         rest_bytes, stream)
+                 : bed_forward_ws_f32(S, batch, n, evals, out, status, nullptr, flags, nullptr,
+                                      nullptr, &cv, rest, rest_bytes, stream);
+  }
+  if (flags) {
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "bed_scatter_forward_f32 memset(flags)");
+  }
+  if (batch == 0) return BED_SUCCESS;
+  // n <= 8: one kernel -- each thread forms its covariance from X in registers,
+  // solves it, and writes evals and V (or the power); S never reaches memory
+  const bed::ScatSpec sc{X, m, eps};
+  const bed::PowSpec spec{p, floor, (p < 0.0f || p != floorf(p)) ? 1 : 0};
+  bed::FwdArgs a{X, batch, n, evals, cv.compute_vectors ? out : nullptr, status, nullptr, flags,
+                 kernel_cfg(&cv, n), s, bed::DiagOut{nullptr, nullptr}, nullptr, 0,
+                 power ? &spec : nullptr, &sc};
+  cudaError_t e = dispatch_forward(a);
+  if (e != cudaSuccess) return cuda_fail(e, "bed_scatter_forward_f32 launch");
+  return BED_SUCCESS;
+}
+
 // Host-buffer entry: the batch streams through the device in chunks.  Three
 // role streams -- host-to-device copies, solves, device-to-host copies --
 // and a ring of kSlots device buffer sets ordered by events, so the copy

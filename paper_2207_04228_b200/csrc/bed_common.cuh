@@ -72,6 +72,15 @@ struct PowSpec {
   int needs_positive;  // p negative or fractional: a non-positive clamped eigenvalue is an error
 };
 
+// Covariance producer fused in front of the forward (bed_scatter_forward_f32):
+// the matrix is formed from X (batch, n, m) as (X - mu)(X - mu)^T + eps I
+// (zca_whiten's scatter, solver.py:161-166) instead of being read.
+struct ScatSpec {
+  const float* X;
+  int m;
+  float eps;
+};
+
 struct KernelCfg {
   float eps;       // deflation_tol
   float sym_tol;   // symmetry_tol

@@ -23,7 +23,8 @@ struct FwdArgs {
   DiagOut dg;       // optional per-matrix diagnostics
   void* ws;         // n >= 9: device workspace (bed_forward_workspace_bytes)
   size_t ws_bytes;  // a smaller workspace solves the batch in chunks
-  const PowSpec* pw = nullptr;  // n <= 8: write the spectral power to evecs instead of V
+  const PowSpec* pw = nullptr;  // write the spectral power to evecs instead of V
+  const ScatSpec* sc = nullptr;  // n <= 8: form A from X (A is ignored)
 };
 
 // Workspace bytes the n >= 9 path needs for `batch` matrices in one chunk

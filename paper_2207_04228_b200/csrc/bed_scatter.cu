@@ -4,7 +4,8 @@
 // scatter of the reference zca_whiten (solver.py:161-166) and of
 // decorrelated BN / global covariance pooling.
 //
-// A CTA owns 128 / (NMAX/4)^2 matrices (one for n > 32): pass 1 reduces the channel means
+// n <= 8 takes the one-thread-per-matrix producer of bed_scatter_regs.cuh.
+// Above, a CTA owns 128 / (NMAX/4)^2 matrices (one for n > 32): pass 1 reduces the channel means
 // (one warp per channel row, coalesced), pass 2 streams the centred
 // samples in chunks of KC through shared memory k-major (X_c^T) and
 // accumulates X_c X_c^T on the 4 x 4 FFMA2 register tiles of the backward
@@ -12,6 +13,7 @@
 // through the stage like the reference ((S + S^T) / 2, solver.py:164).
 #include "bed_backward.cuh"
 #include "bed_launch.h"
+#include "bed_scatter_regs.cuh"
 
 namespace bed {
 
@@ -154,9 +156,25 @@ static cudaError_t go_scatter(const ScatArgs& a) {
   return cudaGetLastError();
 }
 
+template <int N>
+static cudaError_t go_scatter_small(const ScatArgs& a) {
+  const unsigned grid = (unsigned)((a.batch + kScatSmallThreads - 1) / kScatSmallThreads);
+  bed_scatter_small_kernel<N><<<grid, kScatSmallThreads, 0, a.stream>>>(a.X, a.out, a.batch, a.m, a.eps);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(const ScatArgs& a) {
-  if (a.n <= 4) return go_scatter<4>(a);
-  if (a.n <= 8) return go_scatter<8>(a);
+  switch (a.n) {  // n <= 8: one thread per matrix (bed_scatter_regs.cuh)
+    case 1: return go_scatter_small<1>(a);
+    case 2: return go_scatter_small<2>(a);
+    case 3: return go_scatter_small<3>(a);
+    case 4: return go_scatter_small<4>(a);
+    case 5: return go_scatter_small<5>(a);
+    case 6: return go_scatter_small<6>(a);
+    case 7: return go_scatter_small<7>(a);
+    case 8: return go_scatter_small<8>(a);
+    default: break;
+  }
   if (a.n <= 16) return go_scatter<16>(a);
   if (a.n <= 32) return go_scatter<32>(a);
   return go_scatter<64>(a);

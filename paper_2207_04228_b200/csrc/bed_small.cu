@@ -7,7 +7,18 @@ namespace bed {
 template <int N>
 static cudaError_t go_small(const FwdArgs& a) {
   const unsigned grid = (unsigned)((a.batch + kSmallThreads - 1) / kSmallThreads);
-  if (a.pw)
+  if (a.sc) {  // covariance producer fused in front (and the power behind, if asked)
+    const PowSpec pw = a.pw ? *a.pw : PowSpec{};
+    if (a.pw)
+      bed_small_kernel<N, true, true, true><<<grid, kSmallThreads, 0, a.stream>>>(
+          a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg, pw, *a.sc);
+    else if (a.evecs)
+      bed_small_kernel<N, true, false, true><<<grid, kSmallThreads, 0, a.stream>>>(
+          a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg, pw, *a.sc);
+    else
+      bed_small_kernel<N, false, false, true><<<grid, kSmallThreads, 0, a.stream>>>(
+          a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg, pw, *a.sc);
+  } else if (a.pw)
     bed_small_kernel<N, true, true><<<grid, kSmallThreads, 0, a.stream>>>(
         a.A, a.batch, a.evals, a.evecs, a.status, a.steps, a.flags, a.cfg, a.dg, *a.pw);
   else if (a.evecs)

@@ -39,6 +39,7 @@
 #pragma once
 
 #include "bed_common.cuh"
+#include "bed_scatter_regs.cuh"
 #include "bed_f32x2.cuh"
 
 namespace bed {
@@ -214,12 +215,17 @@ __device__ __forceinline__ int small_deflate_zero(float (&e)[N], int m, float ep
 // solver.py:115-143) is formed from V in registers and written to `evecs` in
 // place of V -- the fused epilogue of SURVEY.md 8(f) row 1; V never leaves
 // the thread.
-template <int N, bool VECS, bool POW = false>
+// SCAT: the thread forms its matrix from X (n channels x m samples) as the
+// scatter (X - mu)(X - mu)^T + eps I (zca_whiten, solver.py:161-166; the
+// covariance producer of SURVEY.md 8(f) row 3) in registers, in one pass
+// shifted by each channel's first sample (as bed_scatter.cu), instead of
+// reading A: the covariance never reaches memory.
+template <int N, bool VECS, bool POW = false, bool SCAT = false>
 __global__ void __launch_bounds__(kSmallThreads)
     bed_small_kernel(const float* __restrict__ A, int64_t batch, float* __restrict__ evals,
                      float* __restrict__ evecs, int32_t* __restrict__ status_out,
                      int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg,
-                     DiagOut dg, PowSpec pw = PowSpec{}) {
+                     DiagOut dg, PowSpec pw = PowSpec{}, ScatSpec sc = ScatSpec{}) {
   static_assert(!POW || VECS, "the power is formed from the eigenvectors");
   using Lay = SmallLayout<N>;
   constexpr int NN = Lay::NN;
@@ -241,7 +247,10 @@ __global__ void __launch_bounds__(kSmallThreads)
   {
     float x[N][N];
     const bool direct = (NN % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-    if (direct) {
+    if constexpr (SCAT) {
+      scatter_regs<N>(sc.X + (base + (live ? tid : 0)) * (int64_t)N * sc.m, sc.m, sc.eps, live,
+                      (reinterpret_cast<uintptr_t>(sc.X) & 15) == 0, x);
+    } else if (direct) {
       if constexpr (NN % 4 == 0) {
         const float4* p = reinterpret_cast<const float4*>(A + (base + (live ? tid : 0)) * NN);
 #pragma unroll

@@ -31,7 +31,8 @@ from .core import (
 
 __all__ = ["batched_eig", "eigh", "BatchedEigFn", "taylor_backward", "forward_into", "workspace",
            "spectral_power", "SpectralPowerFn", "power_of",
-           "matrix_power", "zca_whiten", "scatter_matrices", "TAYLOR_DEGREE"]
+           "matrix_power", "zca_whiten", "scatter_matrices",
+           "scatter_eig", "scatter_power", "TAYLOR_DEGREE"]
 
 TAYLOR_DEGREE = 9
 
@@ -99,8 +100,9 @@ def _raise_for_status(A: torch.Tensor, status: torch.Tensor, flags: int, cfg: So
     st = status.cpu()
     if flags & (1 << _native.STATUS_NON_FINITE):
         k = int(torch.nonzero(st == _native.STATUS_NON_FINITE)[0, 0])
-        bad = torch.nonzero(~torch.isfinite(A[k].detach().cpu()))[0]
-        raise NonFinite(k, (int(bad[0]), int(bad[1])))
+        bad = torch.nonzero(~torch.isfinite(A[k].detach().cpu()))
+        # (-1, -1): the input is finite but a matrix formed from it overflowed
+        raise NonFinite(k, (int(bad[0, 0]), int(bad[0, 1])) if len(bad) else (-1, -1))
     if flags & (1 << _native.STATUS_NON_SYMMETRIC):
         k = int(torch.nonzero(st == _native.STATUS_NON_SYMMETRIC)[0, 0])
         a = A[k].detach().double().cpu()
@@ -324,6 +326,62 @@ def scatter_matrices(x: torch.Tensor, eps: float = 0.0) -> torch.Tensor:
     return out
 
 
+def _scatter_forward(x, eps, cfg, power, p, floor, check):
+    cfg = cfg or SolverConfig()
+    if eps < 0:
+        raise ValueError("eps must be nonnegative")
+    x = _check_cuda_f32(x, "X")
+    b, n, m = x.shape
+    if m < 1:
+        raise ValueError("X needs at least one sample")
+    c = _native.make_config(cfg, n)
+    vecs = power or cfg.compute_vectors
+    dev = x.device
+    evals = torch.empty((b, n), device=dev, dtype=torch.float32)
+    out = torch.empty((b, n, n), device=dev, dtype=torch.float32) if vecs else None
+    status = torch.empty((b,), device=dev, dtype=torch.int32)
+    flags = torch.empty((1,), device=dev, dtype=torch.int32)
+    wb = _native.scatter_forward_workspace_bytes(b, n, m, c, power)
+    ws = torch.empty((wb + 256,), dtype=torch.uint8, device=dev) if wb else None
+    wp = ((ws.data_ptr() + 255) & ~255) if ws is not None else None
+    with torch.cuda.device(dev):
+        _native.scatter_forward_f32(x.data_ptr(), b, n, m, float(eps), evals.data_ptr(),
+                                    out.data_ptr() if out is not None else None, status.data_ptr(),
+                                    flags.data_ptr(), c, power, float(p),
+                                    -1.0 if floor is None else float(floor), wp, wb,
+                                    _stream_handle(dev))
+    if check:
+        fl = int(flags.item())
+        _raise_for_status(x, status, fl & ~(1 << _native.STATUS_NON_POSITIVE), cfg)
+        if fl & (1 << _native.STATUS_NON_POSITIVE):
+            k = int(torch.nonzero(status == _native.STATUS_NON_POSITIVE)[0, 0])
+            raise NonPositiveSpectrum(k, float(evals[k].min()))
+    return evals, out
+
+
+def scatter_eig(x: torch.Tensor, eps: float = 0.0, cfg: SolverConfig | None = None,
+                check: bool = True):
+    """Eigen-decomposition of the scatter matrices of a (batch, n, m) CUDA
+    float32 batch (``scatter_matrices`` then ``batched_eig``; reference
+    zca_whiten's scatter + batched_eig, solver.py:79-112,161-166) in one call
+    (C ABI ``bed_scatter_forward_f32``): for n <= 8 one kernel forms each
+    covariance in registers and solves it, so it never reaches memory.
+    Returns (evals, evecs); evecs is None when ``cfg.compute_vectors`` is off.
+    A non-finite sample raises NonFinite at its (channel, sample) position."""
+    return _scatter_forward(x, eps, cfg, 0, 0.0, None, check)
+
+
+def scatter_power(x: torch.Tensor, p: float, eps: float = 0.0, cfg: SolverConfig | None = None,
+                  floor: float | None = None, check: bool = True) -> torch.Tensor:
+    """S^p = V diag(max(lambda, floor)^p) V^T of the scatter matrices
+    S = (X - mu)(X - mu)^T + eps I of a (batch, n, m) CUDA float32 batch, in
+    one call (``bed_scatter_forward_f32`` with power): for n <= 8 a single
+    kernel goes from X to S^p -- neither S nor V reaches memory (the whitening
+    matrix of decorrelated BN / zca_whiten, solver.py:146-169, with p = -1/2).
+    Raises like ``power_of``."""
+    return _scatter_forward(x, eps, cfg, 1, p, floor, check)[1]
+
+
 def _power_values(lam: torch.Tensor, p: float, floor: float | None):
     """f(lambda) = max(lambda, floor)^p and f'(lambda) (0 where the floor
     clamps), the floor resolved per matrix like bed_matrix_power_f32:
@@ -425,10 +483,11 @@ def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None
     ``zca_whiten``, solver.py:146-169): the unnormalised scatter
     (X - mu)(X - mu)^T + eps_reg I is decomposed on the GPU and its inverse
     square root (``matrix_power(-0.5, floor=0)``) applied to the centred
-    features.  The scatter is the native covariance producer
-    (``scatter_matrices`` / ``bed_scatter_f32``), the ED and the inverse
-    square root are the native kernels, and the final product
-    ``A^(-1/2) (X - mu)`` is a torch batched matmul.
+    features.  Scatter, ED and inverse square root are one native call
+    (``scatter_power`` / ``bed_scatter_forward_f32``: a single kernel for
+    n <= 8, the covariance producer + the forward with the power fused into
+    its epilogue above); the final product ``S^(-1/2) (X - mu)`` is a torch
+    batched matmul.
     """
     if eps_reg < 0:
         raise ValueError("eps_reg must be nonnegative")
@@ -437,14 +496,7 @@ def zca_whiten(x: BatchedMatrix, eps_reg: float, cfg: SolverConfig | None = None
     t = torch.from_numpy(np.asarray(data, dtype=np.float32)) if host else data
     if host:
         t = t.to(torch.device("cuda", torch.cuda.current_device()))
-    finite = torch.isfinite(t)
-    if not bool(finite.all()):
-        b, i, j = (int(v) for v in torch.nonzero(~finite)[0])
-        raise NonFinite(b, (i, j))
     t = t.contiguous()
-    scatter = scatter_matrices(t, eps_reg)
-    centered = t - t.mean(dim=2, keepdim=True)
-    dec = batched_eig(scatter, cfg)
-    inv_root = matrix_power(dec, -0.5, floor=0.0).data
-    out = inv_root @ centered
+    inv_root = scatter_power(t, -0.5, eps_reg, cfg, floor=0.0)
+    out = inv_root @ (t - t.mean(dim=2, keepdim=True))
     return BatchedMatrix(out.cpu().numpy().astype(np.float64) if host else out)

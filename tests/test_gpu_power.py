@@ -273,3 +273,102 @@ def test_power_of_errors_and_default_floor(bed, n):
     with torch.no_grad():
         y = bed.spectral_power(x, -0.5)
     np.testing.assert_allclose(y.cpu().numpy(), bed.power_of(x, -0.5).cpu().numpy(), rtol=0, atol=0)
+
+
+# ---- covariance -> ED [-> power] in one call (bed_scatter_forward_f32; one kernel for n <= 8)
+
+
+def _samples(b, n, m, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((b, n, m)) * 2.0 + rng.standard_normal((b, n, 1)) * 5.0).astype(np.float32)
+
+
+def _scatter64(x, eps):
+    xc = x.astype(np.float64) - x.astype(np.float64).mean(axis=2, keepdims=True)
+    s = xc @ xc.transpose(0, 2, 1)
+    return (s + s.transpose(0, 2, 1)) / 2 + eps * np.eye(x.shape[1])
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (1, 6), (2, 3), (3, 12), (4, 16), (4, 17), (5, 20), (6, 8),
+                                 (7, 29), (8, 32), (8, 5), (9, 36), (16, 64), (24, 50), (40, 160)])
+def test_scatter_eig_matches_float64(bed, n, m):
+    b, eps = 333, 1e-2  # 333: a partial last CTA
+    x = _samples(b, n, m, 7 * n + m)
+    cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n)
+    lam, v = bed.scatter_eig(torch.from_numpy(x).cuda(), eps, cfg)
+    lam, v = lam.cpu().numpy().astype(np.float64), v.cpu().numpy().astype(np.float64)
+    s = _scatter64(x, eps)
+    ref = np.linalg.eigvalsh(s)[:, ::-1]
+    scale = np.linalg.norm(s, axis=(1, 2))
+    assert (np.abs(lam - ref).max(axis=1) / scale).max() <= 1e-5
+    rec = (v * lam[:, None, :]) @ v.transpose(0, 2, 1)
+    assert (np.linalg.norm(rec - s, axis=(1, 2)) / scale).max() <= 2e-5
+    eye = np.eye(n)
+    assert np.abs(v.transpose(0, 2, 1) @ v - eye).max() <= 1e-5
+    # evals-only and the A-input path agree with the fused one on the same X
+    cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n, compute_vectors=False)
+    lam2, v2 = bed.scatter_eig(torch.from_numpy(x).cuda(), eps, cfg)
+    assert v2 is None
+    np.testing.assert_allclose(lam2.cpu().numpy(), lam, rtol=0, atol=1e-5 * scale.max())
+
+
+@pytest.mark.parametrize("n,m", [(1, 4), (2, 9), (3, 12), (4, 16), (4, 31), (6, 24), (8, 32),
+                                 (8, 64), (12, 48), (16, 64), (32, 128), (48, 192)])
+@pytest.mark.parametrize("p", [-0.5, 0.5, -1.0])
+def test_scatter_power_matches_float64(bed, n, m, p):
+    b, eps = 200, 1e-1
+    x = _samples(b, n, m, 11 * n + m)
+    cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n)
+    got = bed.scatter_power(torch.from_numpy(x).cuda(), p, eps, cfg, floor=0.0).cpu().numpy()
+    s = _scatter64(x, eps)
+    w, q = np.linalg.eigh(s)
+    ref = (q * w[:, None, :] ** p) @ q.transpose(0, 2, 1)
+    err = np.linalg.norm(got.astype(np.float64) - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
+    cond = w[:, -1] / w[:, 0]
+    # FP32: input rounding of S amplified by the condition number (to the |p|-ish power)
+    assert (err / (1.0 + cond) ** max(abs(p), 0.5)).max() <= 2e-6, (err.max(), cond.max())
+    np.testing.assert_array_equal(got, got.transpose(0, 2, 1))
+
+
+@pytest.mark.parametrize("n", [3, 4, 8, 16])
+def test_scatter_power_equals_composed_path(bed, n):
+    """The fused call and scatter_matrices -> power_of on the same X: same
+    matrix up to the producer's rounding (both shift by the first sample).
+    Budget 4n (the reference's verify profile, bench.py:227-228): under the
+    default 2n a few of these scatters need 7 double steps at n = 3 -- the
+    float64 oracle too (oracle.forward(max_double_steps=6) reports them)."""
+    x = torch.from_numpy(_samples(500, n, 8 * n, n)).cuda()
+    cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n)
+    fused = bed.scatter_power(x, -0.5, 1e-2, cfg, floor=0.0)
+    composed = bed.power_of(bed.scatter_matrices(x, 1e-2), -0.5, cfg, floor=0.0)
+    err = torch.linalg.matrix_norm((fused - composed).double()) / torch.linalg.matrix_norm(composed.double())
+    assert float(err.max()) <= 1e-4
+
+
+@pytest.mark.parametrize("n", [4, 7, 16])
+def test_scatter_forward_layouts_and_errors(bed, n):
+    m = 4 * n
+    base = torch.from_numpy(_samples(65, n, m + 1, n)).cuda()
+    # misaligned, non-multiple-of-4 rows: X a view one float in (the scalar load path)
+    flat = torch.empty(65 * n * m + 1, device="cuda")
+    flat[1:] = base[:, :, :m].reshape(-1)
+    xm = flat[1:].view(65, n, m)
+    cfg = bed.SolverConfig(deflation_tol=3e-12, max_double_steps=4 * n)
+    a, _ = bed.scatter_eig(xm, 1e-2, cfg)
+    b_, _ = bed.scatter_eig(base[:, :, :m].contiguous(), 1e-2, cfg)
+    torch.testing.assert_close(a, b_, rtol=0, atol=1e-5 * float(b_.abs().max()))
+    # empty batch
+    lam, v = bed.scatter_eig(torch.empty(0, n, m, device="cuda"), 0.0)
+    assert lam.shape == (0, n) and v.shape == (0, n, n)
+    # a NaN sample: NonFinite at its (channel, sample) position, first bad matrix
+    bad = base[:, :, :m].contiguous()
+    bad[40, n - 1, 3] = float("nan")
+    bad[50, 0, 0] = float("inf")
+    with pytest.raises(bed.NonFinite) as err:
+        bed.scatter_power(bad, -0.5, 1e-2)
+    assert err.value.batch_index == 40 and tuple(err.value.position) == (n - 1, 3)
+    # one sample, eps = 0: the scatter is exactly zero -- no positive spectrum for the inverse root
+    with pytest.raises(bed.NonPositiveSpectrum):
+        bed.scatter_power(base[:, :, :1].contiguous(), -0.5, 0.0, floor=0.0)
+    with pytest.raises(ValueError):
+        bed.scatter_eig(base, -1.0)
