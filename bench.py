@@ -62,6 +62,9 @@ def work_per_matrix(n: int, mode: str):
         return f_fwd + 2 * n ** 3, b_fwd + 4 * (2 * n * n + n)
     if mode == "powf":  # eigenvalues + A^p in one call: V never returned (bed_forward_power_f32)
         return f_fwd + 2 * n ** 3, b_fwd
+    if mode == "scatpow":  # X (n x 4n samples) -> S^p and eigenvalues (bed_scatter_forward_f32)
+        m = 4 * n
+        return n * (n + 1) * m + f_fwd + 2 * n ** 3, 4 * (n * m + n * n + n)
     f_bwd = 6 * n ** 3 + 22 * n * n
     b_bwd = 4 * (3 * n * n + 2 * n)
     return f_fwd + f_bwd, b_fwd + b_bwd
@@ -145,7 +148,11 @@ class Step:
 
     def __init__(self, torch, bed, n, batch, mode, dev, seed):
         self.torch, self.bed, self.n, self.batch, self.mode = torch, bed, n, batch, mode
-        self.a = make_inputs(torch, n, batch, mode, seed, dev)
+        if mode == "scatpow":  # samples, not matrices: the covariance is formed inside
+            g = torch.Generator(device=dev).manual_seed(seed)
+            self.a = torch.randn((batch, n, 4 * n), device=dev, generator=g)
+        else:
+            self.a = make_inputs(torch, n, batch, mode, seed, dev)
         self.cfg = bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n,
                                     compute_vectors=mode != "val")
         self.lam = torch.empty((batch, n), device=dev)
@@ -159,7 +166,16 @@ class Step:
             g = torch.Generator(device=dev).manual_seed(seed + 1)
             self.gv = torch.randn((batch, n, n), device=dev, generator=g)
             self.gl = torch.randn((batch, n), device=dev, generator=g)
-        self.ws = bed.workspace(self.a, self.cfg)  # n >= 9: allocated once, outside the timed steps
+        # n >= 9: allocated once, outside the timed steps
+        self.ws = bed.workspace(self.a, self.cfg) if mode != "scatpow" else None
+        if mode == "scatpow":
+            from paper_2207_04228_b200 import _native
+
+            self.pws_bytes = _native.scatter_forward_workspace_bytes(batch, n, 4 * n,
+                                                                     _native.make_config(self.cfg, n), 1)
+            self.pws = torch.empty((self.pws_bytes + 256,), dtype=torch.uint8, device=dev)
+            self.pws_ptr = (self.pws.data_ptr() + 255) & ~255 if self.pws_bytes else None
+            self.steps.zero_()
         if mode == "powf":
             from paper_2207_04228_b200 import _native
 
@@ -167,9 +183,21 @@ class Step:
             self.pws = torch.empty((self.pws_bytes + 256,), dtype=torch.uint8, device=dev)
             self.pws_ptr = (self.pws.data_ptr() + 255) & ~255 if self.pws_bytes else None
             self.steps.zero_()
-        self.launches = 1 if mode in ("fwd", "val") or (mode == "powf" and n <= 8) else 2
+        self.launches = 1 if mode in ("fwd", "val") or (mode in ("powf", "scatpow") and n <= 8) else 2
+        if mode == "scatpow" and n > 8:
+            self.launches = 3 if n > 24 else 2  # scatter, forward (+ power kernel above n = 24)
 
     def __call__(self):
+        if self.mode == "scatpow":  # S^(-1/2) of the samples' scatter: the whitening matrix
+            from paper_2207_04228_b200 import _native
+
+            c = _native.make_config(self.cfg, self.n)
+            _native.scatter_forward_f32(self.a.data_ptr(), self.batch, self.n, 4 * self.n, 1e-3,
+                                        self.lam.data_ptr(), self.vec.data_ptr(),
+                                        self.status.data_ptr(), None, c, 1, -0.5, -1.0,
+                                        self.pws_ptr, self.pws_bytes,
+                                        self.torch.cuda.current_stream().cuda_stream)
+            return
         if self.mode == "powf":
             from paper_2207_04228_b200 import _native
 
@@ -435,7 +463,8 @@ def other_configs(torch, bed, dev, hbm_peak):
              (64, 8192, "fwd"), (16, 65536, "fwdbwd"), (64, 8192, "fwdbwd"),
              (16, 65536, "fwdpow"), (64, 8192, "fwdpow"),
              (4, 1 << 22, "val"), (16, 1 << 18, "val"), (32, 1 << 16, "val"), (64, 8192, "val"),
-             (4, 1 << 22, "fwdpow"), (4, 1 << 22, "powf"), (16, 65536, "powf")]
+             (4, 1 << 22, "fwdpow"), (4, 1 << 22, "powf"), (16, 65536, "powf"),
+             (4, 1 << 20, "scatpow"), (8, 1 << 18, "scatpow"), (16, 65536, "scatpow")]
     for n, b, mode in cases:
         st = Step(torch, bed, n, b, mode, dev, seed=n)
         reps = 50 if b <= 4096 else 10

@@ -19,6 +19,20 @@ if "scat" in sys.argv:  # covariance producer only
     torch.cuda.synchronize()
     print("done")
     sys.exit(0)
+if "powf" in sys.argv or "scatpow" in sys.argv:  # the fused power / covariance paths
+    for n, b, _ in cases:
+        if which and str(n) not in which:
+            continue
+        if "powf" in sys.argv:
+            a = covariance_device(b, n, 4 * n, 0)
+            bed.power_of(a, -0.5, check=False)
+        else:
+            x = torch.randn((b // 4, n, 4 * n), device="cuda")
+            bed.scatter_power(x, -0.5, 1e-3, check=False)
+            bed.scatter_matrices(x, 1e-3)
+    torch.cuda.synchronize()
+    print("done")
+    sys.exit(0)
 for n, b, bwd in cases:
     if which and str(n) not in which:
         continue

@@ -15,6 +15,10 @@ bash tools/ncu_export.sh bwd16 "bed_backward_kernel" 0 python tools/profile_case
 bash tools/ncu_export.sh bwd64 "bed_backward_kernel" 0 python tools/profile_cases.py 64
 bash tools/ncu_export.sh pow16 "bed_power_kernel" 0 python tools/profile_cases.py 16 pow
 bash tools/ncu_export.sh scat16 "bed_scatter_kernel" 0 python tools/profile_cases.py scat
+bash tools/ncu_export.sh powf4 "bed_small_kernel" 0 python tools/profile_cases.py 4 powf
+bash tools/ncu_export.sh powf16 "bed_fold_tma_kernel" 0 python tools/profile_cases.py 16 powf
+bash tools/ncu_export.sh scatpow4 "bed_small_kernel" 0 python tools/profile_cases.py 4 scatpow
+bash tools/ncu_export.sh scatsmall4 "bed_scatter_small_kernel" 0 python tools/profile_cases.py 4 scatpow
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cases.csv \
     python tools/profile_cases.py > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv \

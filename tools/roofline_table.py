@@ -6,6 +6,9 @@ Work model (the formulas bench.py uses):
   forward  F = (8/3) n^3 + (6n + 24) n (n - 1) flops, B = 4 (2 n^2 + n) bytes
   backward F = 6 n^3 + 22 n^2,                          B = 4 (3 n^2 + 2 n)
   power    F = 2 n^3,                                    B = 4 (2 n^2 + n)
+  modes: fwd, val (eigenvalues only), fwdbwd, fwdpow (forward + power kernel), powf
+  (eigenvalues + A^p in one call), scatpow (X of 4n samples -> S^p in one call,
+  + n (n + 1) 4n scatter flops, B = 4 (4 n^2 + n^2 + n)) -- bench.work_per_matrix
 Roofline time = max(B / HBM, F / FP32) with HBM from MEASURED_PEAKS.json and
 FP32 = 73.7 TFLOP/s (measured FFMA2 peak, profiles/r01_fp32_peak.md)."""
 import json
