@@ -297,8 +297,9 @@ def e2e_host(torch, bed, n, batch, steps, dev_index):
 def e2e_numpy_api(bed, n, batch, steps):
     """The reference-facing Python call exactly as a reference user makes it:
     batched_eig(BatchedSymmetric(float64 numpy)) -> float64 numpy results
-    (solver.py:79-112): host float64 validation + symmetrisation, FP32 cast
-    into page-locked memory, H2D, solve, D2H, float64 results -- all timed."""
+    (solver.py:79-112) -> bed_forward_host_f64: float64 validation +
+    symmetrisation and the FP32 cast on host threads into page-locked staging,
+    H2D, solve, D2H, float64 results -- all timed, chunks overlapped."""
     import oracle
 
     a = oracle.gen_spd(min(batch, 1 << 20), n, 7)
@@ -312,9 +313,11 @@ def e2e_numpy_api(bed, n, batch, steps):
     sec = statistics.median(times)
     b = a.shape[0]
     return {"value": b / sec, "unit": UNIT, "batch": b, "h2d_bytes_per_step": 4 * b * n * n,
-            "d2h_bytes_per_step": 4 * b * (n * n + n) + 16 * b,
-            "path": "batched_eig(BatchedSymmetric(float64 numpy)), median of "
-                    f"{steps} calls (host float64 validate + cast dominate)"}
+            "d2h_bytes_per_step": 4 * b * (n * n + n) + 24 * b,
+            "host_threads": min(os.cpu_count() or 1, 64),
+            "path": "batched_eig(BatchedSymmetric(float64 numpy)) -> C ABI bed_forward_host_f64 "
+                    f"(host-thread float64 validate/cast overlapped with PCIe and the solve), median of "
+                    f"{steps} calls"}
 
 
 def load_traffic(name):
@@ -447,7 +450,9 @@ def torch_eigh_ms(torch, a, reps=3):
                 if ms > 500.0:
                     break
             return best
-        except Exception:  # noqa: BLE001
+        except Exception as e:  # noqa: BLE001
+            print(f"torch.linalg.eigh chunk={chunked} on {tuple(a.shape)}: {type(e).__name__}: "
+                  f"{str(e)[:200]}", file=sys.stderr)
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
     return None

@@ -34,6 +34,8 @@
  *                          householder.py:190-192, qr.py:601-602)
  *   bed_forward_host_f32   the same call on host (numpy-side) buffers, the
  *                          way the reference API is called (solver.py:79)
+ *   bed_forward_host_f64   the same on float64 host buffers with the reference's
+ *                          float64 validate (core.py:286-309) on host threads
  *   bed_backward_f32       (absent in the reference: pkg/README.md:116-117)
  *                          ED backward with Taylor-K
  *   bed_forward_power_f32  batched_eig() + matrix_power() in one call, fused into the
@@ -164,6 +166,21 @@ int bed_backward_f32(const float* V, const float* evals, const float* gV, const 
 int bed_matrix_power_f32(const float* V, const float* evals, float* out, int32_t* status,
                          int32_t* flags, int64_t batch, int32_t n, float p, float floor,
                          void* stream);
+
+/* The float64 host call a reference user makes (batched_eig on float64 numpy,
+ * solver.py:79-112): A, evals, evecs are HOST float64 buffers (pageable is fine).
+ * Host threads validate each matrix as the reference does (core.py:286-309:
+ * finite, max|a_ij - a_ji| <= symmetry_tol * max(1, ||A||_F), then (A + A^T) / 2,
+ * all in float64), cast it to FP32 into page-locked staging, and the chunks
+ * stream through the device (one stream per staging slot) while the threads
+ * convert the next chunk in and the previous one out.  A matrix rejected on the
+ * host gets BED_STATUS_NON_FINITE / _NON_SYMMETRIC and the zero matrix's results.
+ * status, steps, diag (batch x 3: rotations, reduction events, step_r_sum), resid
+ * are host arrays, nullable.  threads <= 0: all hardware threads (<= 64).  Calls
+ * for the same device serialise on its staging buffer (kept between calls). */
+int bed_forward_host_f64(const double* A, int64_t batch, int32_t n, double* evals, double* evecs,
+                         int32_t* status, int32_t* steps, int32_t* diag, float* resid,
+                         const bed_config* cfg, int32_t device, int32_t threads);
 
 /* Eigenvalues and the spectral power  out = V diag(max(evals, floor)^p) V^T  in one
  * call (reference batched_eig + matrix_power, solver.py:79-143),

@@ -26,6 +26,7 @@ EXPORTS = (
     "bed_forward_ws_f32",
     "bed_forward_workspace_bytes",
     "bed_forward_host_f32",
+    "bed_forward_host_f64",
     "bed_backward_f32",
     "bed_matrix_power_f32",
     "bed_forward_power_f32",
@@ -81,6 +82,9 @@ def lib() -> ctypes.CDLL:
     L.bed_forward_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(BedConfig)]
     L.bed_forward_host_f32.restype = ctypes.c_int
     L.bed_forward_host_f32.argtypes = [vp, i64, i32, vp, vp, vp, vp, ctypes.POINTER(BedConfig), i32]
+    L.bed_forward_host_f64.restype = ctypes.c_int
+    L.bed_forward_host_f64.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp,
+                                       ctypes.POINTER(BedConfig), i32, i32]
     L.bed_backward_f32.restype = ctypes.c_int
     L.bed_backward_f32.argtypes = [vp, vp, vp, vp, vp, i64, i32, i32, vp, vp, vp]
     L.bed_matrix_power_f32.restype = ctypes.c_int
@@ -160,6 +164,13 @@ def forward_host_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_pt
     rc = lib().bed_forward_host_f32(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr,
                                     ctypes.byref(cfg), device)
     check(rc, "bed_forward_host_f32")
+
+
+def forward_host_f64(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr, diag_ptr,
+                     resid_ptr, cfg: BedConfig, device: int, threads: int = 0) -> None:
+    rc = lib().bed_forward_host_f64(A_ptr, batch, n, evals_ptr, evecs_ptr, status_ptr, steps_ptr,
+                                    diag_ptr, resid_ptr, ctypes.byref(cfg), device, threads)
+    check(rc, "bed_forward_host_f64")
 
 
 def matrix_power_f32(V_ptr, evals_ptr, out_ptr, status_ptr, flags_ptr, batch, n, p, floor,

@@ -7,8 +7,11 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <omp.h>
+
 #include <algorithm>
 #include <mutex>
+#include <thread>
 
 #include "../../include/bed200.h"
 #include "bed_launch.h"
@@ -408,7 +411,7 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
     for (int b = 0; b < kSlots && out == BED_SUCCESS; ++b)
       if ((e = cudaEventCreateWithFlags(&ev[r][b], cudaEventDisableTiming)) != cudaSuccess) out = cuda_fail(e, "event");
   }
-  const size_t wsb = n > 8 ? std::max(bed_forward_workspace_bytes(chunk, n, cfg), (size_t)0) : 0;
+  const size_t wsb = bed_forward_workspace_bytes(chunk, n, cfg);
   if (out == BED_SUCCESS && (e = pool_alloc(reinterpret_cast<void**>(&pool), slot * kSlots + wsb, st[C])) != cudaSuccess)
     out = cuda_fail(e, "bed_forward_host_f32 allocation");
   if (out == BED_SUCCESS && (e = cudaEventRecord(ev[C][0], st[C])) == cudaSuccess) {
@@ -458,6 +461,210 @@ int bed_forward_host_f32(const float* A, int64_t batch, int32_t n, float* evals,
       if (ev[r][b]) cudaEventDestroy(ev[r][b]);
     if (st[r]) cudaStreamDestroy(st[r]);
   }
+  cudaSetDevice(prev);
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Float64 host-buffer entry -- the call a reference user makes
+// (batched_eig(BatchedSymmetric(float64 numpy)), solver.py:79-112).  The
+// reference validates in float64 (core.py:286-309); here host threads do the
+// same per matrix -- finiteness, max|a - a^T| <= symmetry_tol * max(1, ||A||_F),
+// (A + A^T) / 2 -- and write the FP32 cast straight into a page-locked staging
+// slot, so the validation, the casts and the PCIe copies all overlap.  Chunks
+// cycle through kSlots slots, each with its own stream (H2D, solve, D2H in
+// order); while the GPU works on chunks it-3..it-1 the host threads convert
+// chunk it in and chunk it-kSlots out (FP32 -> float64 into the caller's
+// arrays).  A matrix the host rejects is solved as the zero matrix (what the
+// device kernels do with an invalid input) and keeps the host status.
+namespace {
+
+struct HostStage {
+  std::mutex mu;  // one f64 host call per device at a time owns the staging memory
+  char* buf = nullptr;
+  size_t bytes = 0;
+};
+
+HostStage g_stage[64];
+
+int host_threads(int32_t req) {
+  if (req > 0) return std::min(req, 256);
+  const unsigned hw = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(hw, 64u));
+}
+
+// reference validate (core.py:286-309) for one matrix; returns the status and
+// writes the symmetrised FP32 cast (zeros when rejected)
+inline int32_t validate_cast(const double* a, int n, double sym_tol, float* o) {
+  const int nn = n * n;
+  bool finite = true;
+  double fro2 = 0.0, asym = 0.0;
+  for (int k = 0; k < nn; ++k) {
+    finite = finite && std::isfinite(a[k]);
+    fro2 += a[k] * a[k];
+  }
+  if (!finite) {
+    memset(o, 0, sizeof(float) * nn);
+    return BED_STATUS_NON_FINITE;
+  }
+  for (int r = 0; r < n; ++r)
+    for (int c = 0; c < r; ++c) asym = std::max(asym, std::fabs(a[r * n + c] - a[c * n + r]));
+  if (asym > sym_tol * std::max(1.0, std::sqrt(fro2))) {
+    memset(o, 0, sizeof(float) * nn);
+    return BED_STATUS_NON_SYMMETRIC;
+  }
+  for (int r = 0; r < n; ++r) {
+    o[r * n + r] = (float)a[r * n + r];
+    for (int c = 0; c < r; ++c) {
+      const float v = (float)((a[r * n + c] + a[c * n + r]) / 2.0);
+      o[r * n + c] = v;
+      o[c * n + r] = v;
+    }
+  }
+  return BED_STATUS_OK;
+}
+
+}  // namespace
+
+int bed_forward_host_f64(const double* A, int64_t batch, int32_t n, double* evals, double* evecs,
+                         int32_t* status, int32_t* steps, int32_t* diag, float* resid,
+                         const bed_config* cfg, int32_t device, int32_t threads) {
+  if (!cfg || batch < 0 || n < 1 || n > 64) return BED_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!A || !evals || (cfg->compute_vectors && !evecs))) return BED_ERR_INVALID_ARGUMENT;
+  {
+    // the FP32 checks of the shared validator (pointer alignment of the f64
+    // buffers is 8 bytes, which implies the 4 the validator asks for)
+    int rc = check_forward(reinterpret_cast<const float*>(A), batch, n,
+                           reinterpret_cast<const float*>(evals), reinterpret_cast<const float*>(evecs), cfg);
+    if (rc) return rc;
+  }
+  if ((reinterpret_cast<uintptr_t>(A) & 7) || (reinterpret_cast<uintptr_t>(evals) & 7) ||
+      (reinterpret_cast<uintptr_t>(evecs) & 7) || !aligned4(status) || !aligned4(steps) ||
+      !aligned4(diag) || !aligned4(resid))
+    return BED_ERR_MISALIGNED;
+  if (batch == 0) return BED_SUCCESS;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return BED_ERR_NO_DEVICE;
+  if (device < 0 || device >= ndev || device >= 64) return BED_ERR_INVALID_ARGUMENT;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int nthr = host_threads(threads);
+
+  const bool vecs = cfg->compute_vectors != 0;
+  const int64_t nn = (int64_t)n * n;
+  // page-locked bytes per matrix: FP32 input, evals, V, status, steps, diag (3), resid, host status
+  const int64_t per = 4 * (nn + n + (vecs ? nn : 0) + 7);
+  const int64_t chunk = std::max<int64_t>(1024, std::min<int64_t>(batch, host_chunk_bytes() / per));
+  constexpr int kSlots = 4;
+  const size_t szA = align_up(sizeof(float) * chunk * nn), szL = align_up(sizeof(float) * chunk * n);
+  const size_t szV = vecs ? align_up(sizeof(float) * chunk * nn) : 0, szI = align_up(sizeof(int32_t) * chunk);
+  const size_t slot = szA + szL + szV + 6 * szI;  // status, steps, diag x3, resid
+  const size_t hslot = slot + szI;                 // + the host status
+  const size_t wsb = bed_forward_workspace_bytes(chunk, n, cfg);
+
+  HostStage& hs = g_stage[device];
+  std::lock_guard<std::mutex> lock(hs.mu);
+  int out = BED_SUCCESS;
+  if (hs.bytes < hslot * kSlots) {
+    if (hs.buf) cudaFreeHost(hs.buf);
+    hs.buf = nullptr;
+    hs.bytes = 0;
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&hs.buf), hslot * kSlots, cudaHostAllocPortable)) != cudaSuccess) {
+      hs.buf = nullptr;
+      cudaSetDevice(prev);
+      return cuda_fail(e, "bed_forward_host_f64 staging");
+    }
+    hs.bytes = hslot * kSlots;
+  }
+  cudaStream_t st[kSlots] = {};
+  cudaEvent_t done[kSlots] = {}, ready = nullptr;
+  char* pool = nullptr;
+  for (int b = 0; b < kSlots && out == BED_SUCCESS; ++b)
+    if ((e = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming)) != cudaSuccess)
+      out = cuda_fail(e, "stream/event");
+  if (out == BED_SUCCESS && (e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming)) != cudaSuccess)
+    out = cuda_fail(e, "event");
+  if (out == BED_SUCCESS && (e = pool_alloc(reinterpret_cast<void**>(&pool), (slot + wsb) * kSlots, st[0])) != cudaSuccess)
+    out = cuda_fail(e, "bed_forward_host_f64 allocation");
+  if (out == BED_SUCCESS && (e = cudaEventRecord(ready, st[0])) != cudaSuccess) out = cuda_fail(e, "record");
+  for (int b = 1; b < kSlots && out == BED_SUCCESS; ++b)
+    if ((e = cudaStreamWaitEvent(st[b], ready, 0)) != cudaSuccess) out = cuda_fail(e, "wait");
+
+  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  const double sym_tol = cfg->symmetry_tol;
+  auto hbase = [&](int b) { return hs.buf + hslot * b; };
+  // results of chunk c (in slot c % kSlots) into the caller's float64 arrays
+  auto drain = [&](int64_t c) {
+    const int b = (int)(c % kSlots);
+    const int64_t off = c * chunk, m = std::min<int64_t>(chunk, batch - off);
+    char* h = hbase(b);
+    const float* hL = reinterpret_cast<const float*>(h + szA);
+    const float* hV = reinterpret_cast<const float*>(h + szA + szL);
+    const int32_t* hS = reinterpret_cast<const int32_t*>(h + szA + szL + szV);
+    const int32_t* hK = hS + szI / 4;
+    const int32_t* hD = hK + szI / 4;  // diag, 3 per matrix (3 szI blocks)
+    const float* hR = reinterpret_cast<const float*>(hD + 3 * (szI / 4));
+    const int32_t* hH = reinterpret_cast<const int32_t*>(hR + szI / 4);
+#pragma omp parallel for num_threads(nthr) schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+      for (int k = 0; k < n; ++k) evals[(off + i) * n + k] = (double)hL[i * n + k];
+      if (vecs)
+        for (int64_t k = 0; k < nn; ++k) evecs[(off + i) * nn + k] = (double)hV[i * nn + k];
+      if (status) status[off + i] = hH[i] != BED_STATUS_OK ? hH[i] : hS[i];
+      if (steps) steps[off + i] = hK[i];
+      if (diag)
+        for (int k = 0; k < 3; ++k) diag[(off + i) * 3 + k] = hD[i * 3 + k];
+      if (resid) resid[off + i] = hR[i];
+    }
+  };
+  for (int64_t it = 0; it < nchunks + kSlots && out == BED_SUCCESS; ++it) {
+    const int b = (int)(it % kSlots);
+    if (it >= kSlots) {  // slot b's previous chunk: wait for its read-back, convert it out
+      if ((e = cudaEventSynchronize(done[b])) != cudaSuccess) { out = cuda_fail(e, "bed_forward_host_f64 sync"); break; }
+      drain(it - kSlots);
+    }
+    if (it >= nchunks) continue;
+    const int64_t off = it * chunk, m = std::min<int64_t>(chunk, batch - off);
+    char* h = hbase(b);
+    float* hA = reinterpret_cast<float*>(h);
+    int32_t* hH = reinterpret_cast<int32_t*>(h + slot);
+#pragma omp parallel for num_threads(nthr) schedule(static)
+    for (int64_t i = 0; i < m; ++i) hH[i] = validate_cast(A + (off + i) * nn, n, sym_tol, hA + i * nn);
+    char* d = pool + (slot + wsb) * b;
+    float* dA = reinterpret_cast<float*>(d);
+    float* dL = reinterpret_cast<float*>(d + szA);
+    float* dV = vecs ? reinterpret_cast<float*>(d + szA + szL) : nullptr;
+    int32_t* dS = reinterpret_cast<int32_t*>(d + szA + szL + szV);
+    int32_t* dK = dS + szI / 4;
+    int32_t* dD = dK + szI / 4;
+    float* dR = reinterpret_cast<float*>(dD + 3 * (szI / 4));
+    // D2H of the contiguous output block [evals .. resid] in one copy
+    const size_t outb = szL + szV + 6 * szI;
+    bed::FwdArgs a{dA, m, n, dL, dV, dS, dK, nullptr, kernel_cfg(cfg, n), st[b], bed::DiagOut{dD, dR},
+                   wsb ? d + slot : nullptr, wsb};
+    if ((e = cudaMemcpyAsync(dA, hA, sizeof(float) * m * nn, cudaMemcpyHostToDevice, st[b])) != cudaSuccess ||
+        (e = dispatch_forward(a)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h + szA, d + szA, outb, cudaMemcpyDeviceToHost, st[b])) != cudaSuccess ||
+        (e = cudaEventRecord(done[b], st[b])) != cudaSuccess) {
+      out = cuda_fail(e, "bed_forward_host_f64 chunk");
+      break;
+    }
+  }
+  for (int b = 0; b < kSlots; ++b)
+    if (st[b]) {
+      e = cudaStreamSynchronize(st[b]);
+      if (e != cudaSuccess && out == BED_SUCCESS) out = cuda_fail(e, "bed_forward_host_f64 sync");
+    }
+  if (pool) cudaFreeAsync(pool, st[0]);
+  if (st[0]) cudaStreamSynchronize(st[0]);
+  for (int b = 0; b < kSlots; ++b) {
+    if (done[b]) cudaEventDestroy(done[b]);
+    if (st[b]) cudaStreamDestroy(st[b]);
+  }
+  if (ready) cudaEventDestroy(ready);
   cudaSetDevice(prev);
   return out;
 }

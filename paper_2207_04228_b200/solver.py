@@ -148,23 +148,6 @@ def _diagnostics(steps, diag=None) -> SolveDiagnostics:
                             reduction_counts=diag[:, 1])
 
 
-def _validate_host(a: np.ndarray, cfg: SolverConfig) -> np.ndarray:
-    """The reference ``validate`` (core.py:286-309) on a float64 host batch:
-    NonFinite at the first non-finite entry, NonSymmetric when max|a - a^T| >
-    symmetry_tol * max(1, ||A||_F), else (A + A^T) / 2."""
-    finite = np.isfinite(a)
-    if not finite.all():
-        b, i, j = (int(x) for x in np.argwhere(~finite)[0])
-        raise NonFinite(b, (i, j))
-    at = a.transpose(0, 2, 1)
-    asym = np.abs(a - at).max(axis=(1, 2))
-    bad = asym > cfg.symmetry_tol * np.maximum(1.0, np.linalg.norm(a, axis=(1, 2)))
-    if bad.any():
-        k = int(np.argmax(bad))
-        raise NonSymmetric(k, float(asym[k]))
-    return (a + at) / 2.0
-
-
 def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
     """Full eigendecomposition of a batch of symmetric matrices (solver.py:79-112).
 
@@ -188,9 +171,9 @@ def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
     if arr.ndim != 3 or arr.shape[1] != arr.shape[2] or arr.shape[0] < 1:
         raise ShapeMismatch(f"expected (batch, n, n) array, got {arr.shape}")
     if arr.dtype != np.float32:
-        # validate + symmetrise in the caller's precision before the FP32 cast
-        # (core.py:286-309): rounding to FP32 can split a_ij and a_ji by an ulp
-        arr = _validate_host(np.asarray(arr, dtype=np.float64), cfg)
+        # float64 (the reference's dtype): validate + symmetrise in float64 on
+        # host threads inside the native call (core.py:286-309), then FP32
+        return _solve_host_f64(np.ascontiguousarray(arr, dtype=np.float64), cfg)
     host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).pin_memory()
     dev = torch.device("cuda", torch.cuda.current_device())
     A = host.to(dev, non_blocking=True)
@@ -201,6 +184,40 @@ def batched_eig(a, cfg: SolverConfig | None = None) -> EigenResult:
     return EigenResult(out_l.numpy().astype(np.float64),
                        None if out_v is None else out_v.numpy().astype(np.float64),
                        _diagnostics(steps.cpu().numpy(), diag.cpu().numpy()))
+
+
+def _solve_host_f64(a: np.ndarray, cfg: SolverConfig) -> EigenResult:
+    """float64 host batch -> float64 host results through ``bed_forward_host_f64``
+    (host-thread validation and casts overlapped with the PCIe copies and the
+    solves), raising in the reference's order: NonFinite over the whole batch
+    first, then NonSymmetric (core.py:297-308), then (strict) NoConvergence."""
+    b, n, _ = a.shape
+    evals = np.empty((b, n), np.float64)
+    evecs = np.empty((b, n, n), np.float64) if cfg.compute_vectors else None
+    status = np.empty((b,), np.int32)
+    steps = np.empty((b,), np.int32)
+    diag = np.empty((b, 3), np.int32)
+    resid = np.empty((b,), np.float32)
+    _native.forward_host_f64(a.ctypes.data, b, n, evals.ctypes.data,
+                             evecs.ctypes.data if evecs is not None else None, status.ctypes.data,
+                             steps.ctypes.data, diag.ctypes.data, resid.ctypes.data,
+                             _native.make_config(cfg, n), torch.cuda.current_device())
+    if (status != 0).any():
+        bad = np.flatnonzero(status == _native.STATUS_NON_FINITE)
+        if len(bad):
+            k = int(bad[0])
+            pos = np.argwhere(~np.isfinite(a[k]))
+            # (-1, -1): finite in float64 but beyond the FP32 range
+            raise NonFinite(k, (int(pos[0, 0]), int(pos[0, 1])) if len(pos) else (-1, -1))
+        bad = np.flatnonzero(status == _native.STATUS_NON_SYMMETRIC)
+        if len(bad):
+            k = int(bad[0])
+            raise NonSymmetric(k, float(np.abs(a[k] - a[k].T).max()))
+        if cfg.strict_convergence:
+            idx = np.flatnonzero(status == _native.STATUS_NO_CONVERGENCE).tolist()
+            if idx:
+                raise NoConvergence(idx, float(resid[idx].max()))
+    return EigenResult(evals, evecs, _diagnostics(steps, diag))
 
 
 def taylor_backward(V: torch.Tensor, evals: torch.Tensor, g_v: torch.Tensor | None,
