@@ -1,0 +1,362 @@
+// bed_backward_tc.cuh -- the Taylor-K ED backward for 33 <= n <= 64 on the
+// 5th-generation tensor cores (tcgen05, accumulators in TMEM), in 3xTF32.
+//
+//   gA = sym( V (F o (V^T gV) + diag(gL)) V^T )      (bed_backward.cuh)
+//
+// Why 3xTF32: a single TF32 pass gives gradients 5-10e-4 off float64 (the gate
+// is 1e-4); splitting every operand x = hi + lo (hi = x with the low 13
+// mantissa bits cleared, lo = x - hi, exact) and accumulating hi*hi + hi*lo +
+// lo*hi in FP32 gives <= 1e-6 (profiles/r02_tf32_accuracy.txt).
+//
+// A CTA (8 warps, two per SM) works on one matrix at a time, persistent over
+// the batch, with 64 x 64 x 8 MMAs (cta_group::1, M = 64: row m of D sits in
+// TMEM lane 32 (m / 16) + m % 16).  The three products are arranged so every
+// intermediate leaves the epilogue in the row-per-thread orientation the next
+// product reads:
+//   P1  D = gV^T V   = M^T      A = gV^T, B = V^T (staged transposed from HBM)
+//   E1  M'^T = (F o M + diag gL)^T, row by row            -> X1 (B of P2)
+//   P2  D = V M'     = W        A = V (staged as is),  B = M'^T
+//   E2  W, row by row                                      -> X2 (A of P3)
+//   P3  D = W V^T    = G        A = W, B = V
+//   E3  G through a padded shared stage, gA = (G + G^T) / 2, coalesced
+// Operands live in shared memory in the canonical K-major no-swizzle layout
+// (8-row x 16-byte core matrices; LBO = 128 B between the two core matrices
+// of one K = 8 step, SBO = 2 KB between 8-row groups), each as hi and lo
+// copies: 3 operands x 2 x 16 KB, two CTAs per SM.  One elected thread issues the 3 x 8 MMAs of
+// a product and commits them to an mbarrier the CTA waits on.
+#pragma once
+
+#include <cstdint>
+
+#include "bed_common.cuh"
+#include "bed_mbar.cuh"
+
+namespace bed {
+
+struct BwdTcParams {
+  static constexpr int THREADS = 256;  // 8 warps: warps w and w + 4 share TMEM lanes, split columns
+  static constexpr int BUF = 64 * 64 * 4;              // one operand copy (hi or lo), bytes
+  static constexpr int OPS = 3;                        // X1 (gV^T -> M'^T -> G stage), X2 (V^T -> W), X3 (V)
+  static constexpr int OFF_LAM = OPS * 2 * BUF;        // lam[64], inv[64], gL[64]
+  static constexpr int OFF_BAR = OFF_LAM + 3 * 64 * 4;
+  static constexpr int OFF_TMEM = OFF_BAR + 8;
+  static constexpr int OFF_OUT = OFF_TMEM + 8;
+  static constexpr size_t BYTES = OFF_OUT + 16;
+  static constexpr int CTAS_PER_SM = 2;
+  static constexpr int SPITCH = 65;                    // G stage row pitch (floats)
+  static_assert(64 * SPITCH * 4 <= 2 * BUF, "G stage fits in X1");
+};
+
+// byte offset of element (row, k) in a K-major no-swizzle operand
+__device__ __forceinline__ uint32_t kmaj_off(int row, int k) {
+  return (uint32_t)((row >> 3) * 2048 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+// shared-memory matrix descriptor, version 1 (sm_100), no swizzle, K-major:
+// LBO = 128 B (the next 4 k), SBO = 2048 B (the next 8 rows).  (MN-major
+// descriptors, which would read the transposes from the same rows, gave no
+// products for kind::tf32 in tools/ubench/umma_probe.cu, so the transposed
+// operands are staged as such.)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((lbo >> 4) & 0x3fffu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fffu) << 32) | ((uint64_t)1 << 46);
+}
+
+// kind::tf32, D = F32, A/B = TF32 (K-major), M = 64, N = 64
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((64u >> 4) << 24);
+constexpr uint32_t kIdescTf32MN = kIdescTf32 | (1u << 15) | (1u << 16);  // probe only
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void proxy_fence_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 16 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// one element of F (bed_backward.cuh): the Taylor series of 1/(l_j - l_i)
+// about the pair's larger eigenvalue, the exact value outside its domain
+// (CHECK = false when every eigenvalue of the pair is positive: always inside)
+template <bool CHECK>
+__device__ __forceinline__ float taylor_f(int i, int j, float li, float lj, float ii_inv, float ij_inv,
+                                          int degree, int n, bool& off) {
+  const bool hf = i < j ? (li >= lj) : (li > lj);
+  const float binv = hf ? ii_inv : ij_inv;
+  const float ratio = (hf ? lj : li) * binv;
+  float poly = 1.0f;
+  if (degree == 9) {  // the paper's degree, unrolled
+#pragma unroll
+    for (int k = 0; k < 9; ++k) poly = fmaf(poly, ratio, 1.0f);
+  } else {
+    for (int k = 0; k < degree; ++k) poly = fmaf(poly, ratio, 1.0f);
+  }
+  float tv = poly * binv;
+  if constexpr (CHECK) {
+    const float big = hf ? li : lj, small = hf ? lj : li;
+    const bool in_domain = (big > 0.0f && (fabsf(ratio) < 1.0f || small == big)) ||
+                           (big == 0.0f && small == 0.0f);
+    if (!in_domain && i != j && i < n && j < n) {
+      tv = big != small ? 1.0f / (big - small) : 0.0f;
+      off = true;
+    }
+  }
+  return i == j ? 0.0f : (hf ? -tv : tv);
+}
+
+// 8 values of an operand row (K-major), hi and lo, as two 16-byte chunks
+__device__ __forceinline__ void store8(uint8_t* hi, uint8_t* lo, int row, int k0, const float (&d)[8]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    float4 xh, xl;
+    xh.x = tf32_hi(d[4 * q]);
+    xh.y = tf32_hi(d[4 * q + 1]);
+    xh.z = tf32_hi(d[4 * q + 2]);
+    xh.w = tf32_hi(d[4 * q + 3]);
+    xl = make_float4(d[4 * q] - xh.x, d[4 * q + 1] - xh.y, d[4 * q + 2] - xh.z, d[4 * q + 3] - xh.w);
+    const uint32_t o = kmaj_off(row, k0 + 4 * q);
+    *reinterpret_cast<float4*>(hi + o) = xh;
+    *reinterpret_cast<float4*>(lo + o) = xl;
+  }
+}
+
+// M = 64 rows sit in TMEM lanes 0-15 of each subpartition: after a 16-column
+// load, lane l (< 16) keeps columns 0-7 and lane l + 16 takes columns 8-15 of
+// the same row, so all 32 lanes share the epilogue work
+__device__ __forceinline__ void split_half(const float (&d)[16], int lane, float (&e)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float up = __shfl_sync(0xffffffffu, d[8 + j], lane & 15);
+    e[j] = lane < 16 ? d[j] : up;
+  }
+}
+
+__global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM)
+    bed_backward_tc_kernel(const float* __restrict__ V, const float* __restrict__ lam,
+                           const float* __restrict__ gV, const float* __restrict__ gL,
+                           float* __restrict__ gA, int64_t batch, int n, int degree,
+                           int32_t* __restrict__ status_out, int32_t* __restrict__ flags) {
+  using P = BwdTcParams;
+  extern __shared__ __align__(1024) uint8_t tc_smem[];
+  uint8_t* const smem = tc_smem;
+  auto buf = [&](int op, int part) { return smem + (2 * op + part) * P::BUF; };
+  float* sLam = reinterpret_cast<float*>(smem + P::OFF_LAM);
+  float* sInv = sLam + 64;
+  float* sGl = sInv + 64;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::OFF_TMEM);
+  int* outside = reinterpret_cast<int*>(smem + P::OFF_OUT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  uint32_t phase = 0;
+  const int nn = n * n;
+  // epilogue geometry (M = 64): row m of D sits in TMEM lane 32 (m / 16) +
+  // m % 16, so warp w reads its subpartition's lanes (w % 4) and keeps lanes
+  // 0-15; warps w and w + 4 split the 64 columns
+  const int sub = warp & 3, ch = warp >> 2;
+  const int r = 16 * sub + (lane & 15);  // row of D this thread holds
+  const int c_lo = 32 * ch;
+  const int c_half = lane < 16 ? 0 : 8;  // split_half: this lane's 8 of each 16 columns
+  const uint32_t trow = tmem + ((uint32_t)(32 * sub) << 16) + (uint32_t)c_lo;
+
+  // D = A B^T over K = 64 (3xTF32)
+  auto issue = [&](int opA, int opB) {
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t a_hi = smem_u32(buf(opA, 0)), a_lo = smem_u32(buf(opA, 1));
+      const uint32_t b_hi = smem_u32(buf(opB, 0)), b_lo = smem_u32(buf(opB, 1));
+      constexpr uint32_t lbo = 128u, sbo = 2048u, step = 256u;
+      constexpr uint32_t idesc = kIdescTf32;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t o = step * kk;
+        umma_tf32(tmem, umma_desc(a_lo + o, lbo, sbo), umma_desc(b_hi + o, lbo, sbo), idesc, kk > 0 ? 1u : 0u);
+        umma_tf32(tmem, umma_desc(a_hi + o, lbo, sbo), umma_desc(b_lo + o, lbo, sbo), idesc, 1u);
+        umma_tf32(tmem, umma_desc(a_hi + o, lbo, sbo), umma_desc(b_hi + o, lbo, sbo), idesc, 1u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(bar))
+                   : "memory");
+    }
+  };
+  auto wait_mma = [&]() {
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+  };
+  auto sync_for_mma = [&]() {  // generic-proxy smem writes -> the tensor core
+    proxy_fence_smem();
+    tc_fence_before();
+    __syncthreads();
+  };
+
+  // ---- stage: X1 = gV^T, X2 = V^T, X3 = V (zero padded to 64), hi/lo.  A
+  // warp covers one 8-row x 4-k core block per step: lane -> (row 8rb +
+  // lane/4, k 4kb + lane%4), so the 32 lanes hit 32 distinct banks.  The next
+  // matrix's loads are issued while this one's last product runs (prefetch),
+  // its stores at the top of the next iteration (stage).
+  constexpr int kStageU = 16;  // 128 core blocks / 8 warps
+  float p_rk[kStageU], p_kr[kStageU], p_g[kStageU], p_l = 0.0f, p_gl = 0.0f;
+  auto prefetch = [&](int64_t mm) {
+    const bool have = mm < batch;
+    const float* vb = V + (have ? mm : 0) * nn;
+    const float* gb = gV ? gV + (have ? mm : 0) * nn : nullptr;
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int c = warp + 8 * u;
+      const int row = 8 * (c >> 4) + (lane >> 2), k = 4 * (c & 15) + (lane & 3);
+      const bool ok = have && row < n && k < n;
+      p_rk[u] = ok ? __ldg(vb + row * n + k) : 0.0f;  // V[row][k]
+      p_kr[u] = ok ? __ldg(vb + k * n + row) : 0.0f;  // V[k][row]
+      p_g[u] = (ok && gb) ? __ldg(gb + k * n + row) : 0.0f;
+    }
+    const bool okl = have && tid < n;
+    p_l = okl ? __ldg(lam + mm * n + tid) : 0.0f;
+    p_gl = (okl && gL) ? __ldg(gL + mm * n + tid) : 0.0f;
+  };
+  prefetch(blockIdx.x);
+  for (int64_t m = blockIdx.x; m < batch; m += gridDim.x) {
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int c = warp + 8 * u;
+      const uint32_t o = kmaj_off(8 * (c >> 4) + (lane >> 2), 4 * (c & 15) + (lane & 3));
+      float x;
+      x = tf32_hi(p_g[u]);
+      *reinterpret_cast<float*>(buf(0, 0) + o) = x;
+      *reinterpret_cast<float*>(buf(0, 1) + o) = p_g[u] - x;
+      x = tf32_hi(p_kr[u]);
+      *reinterpret_cast<float*>(buf(1, 0) + o) = x;
+      *reinterpret_cast<float*>(buf(1, 1) + o) = p_kr[u] - x;
+      x = tf32_hi(p_rk[u]);
+      *reinterpret_cast<float*>(buf(2, 0) + o) = x;
+      *reinterpret_cast<float*>(buf(2, 1) + o) = p_rk[u] - x;
+    }
+    bool pos = true;
+    if (tid < 64) {
+      const float l = p_l;
+      sLam[tid] = l;
+      sInv[tid] = l != 0.0f ? 1.0f / l : 0.0f;
+      sGl[tid] = p_gl;
+      pos = tid >= n || l > 0.0f;
+      if (tid == 0) outside[0] = 0;
+    }
+    proxy_fence_smem();
+    tc_fence_before();
+    // every eigenvalue positive: F needs no domain checks
+    const bool all_pos = __syncthreads_and(pos) != 0;
+
+    // ---- P1: D = gV^T V = M^T;  E1: M'^T[r][c] = F(c, r) M[c][r] + (c == r) gL[r] -> X1
+    issue(0, 1);
+    wait_mma();
+    {
+      bool off = false;
+      const float lr = sLam[r], ir = sInv[r];
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const int cb = c_lo + 16 * q + c_half;
+        float d[16], e[8];
+        tmem_ld16(trow + 16u * q, d);
+        tmem_wait_ld();
+        split_half(d, lane, e);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = cb + j;
+          const float lc = sLam[c], icv = sInv[c];
+          const float f = all_pos ? taylor_f<false>(c, r, lc, lr, icv, ir, degree, n, off)
+                                  : taylor_f<true>(c, r, lc, lr, icv, ir, degree, n, off);
+          e[j] = f * e[j] + (c == r ? sGl[r] : 0.0f);
+        }
+        store8(buf(0, 0), buf(0, 1), r, cb, e);
+      }
+      if (off) atomicOr(&outside[0], 1);
+    }
+    sync_for_mma();
+    // ---- P2: D = V M' = W;  E2: W -> X2 (A of P3)
+    issue(2, 0);
+    wait_mma();
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      float d[16], e[8];
+      tmem_ld16(trow + 16u * q, d);
+      tmem_wait_ld();
+      split_half(d, lane, e);
+      store8(buf(1, 0), buf(1, 1), r, c_lo + 16 * q + c_half, e);
+    }
+    sync_for_mma();
+    // ---- P3: D = W V^T = G;  E3: G through the X1 region (free since P2)
+    issue(1, 2);
+    prefetch(m + gridDim.x);  // in flight during P3, E3 and the stores
+    wait_mma();
+    float* sg = reinterpret_cast<float*>(buf(0, 0));
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      float d[16], e[8];
+      tmem_ld16(trow + 16u * q, d);
+      tmem_wait_ld();
+      split_half(d, lane, e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sg[r * P::SPITCH + c_lo + 16 * q + c_half + j] = e[j];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      const int st = outside[0] ? kStatusNonPositive : kStatusOk;
+      if (status_out) status_out[m] = st;
+      if (flags && st) atomicOr(flags, 1 << st);
+    }
+    // gA = (G + G^T) / 2, one row per warp step, coalesced along columns
+    for (int rr = warp; rr < n; rr += P::THREADS / 32) {
+      float* dst = gA + m * nn + rr * n;
+      for (int cc = lane; cc < n; cc += 32) dst[cc] = 0.5f * (sg[rr * P::SPITCH + cc] + sg[cc * P::SPITCH + rr]);
+    }
+    __syncthreads();  // the stage (X1) is rewritten by the next matrix
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
+}
+
+}  // namespace bed
