@@ -349,7 +349,10 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
     // gA = (G + G^T) / 2, one row per warp step, coalesced along columns
     for (int rr = warp; rr < n; rr += P::THREADS / 32) {
       float* dst = gA + m * nn + rr * n;
-      for (int cc = lane; cc < n; cc += 32) dst[cc] = 0.5f * (sg[rr * P::SPITCH + cc] + sg[cc * P::SPITCH + rr]);
+      const float* grow = sg + rr * P::SPITCH;
+      const float* gcol = sg + rr;
+      dst[lane] = 0.5f * (grow[lane] + gcol[lane * P::SPITCH]);  // n > 32: lanes 0..31 all valid
+      if (lane + 32 < n) dst[lane + 32] = 0.5f * (grow[lane + 32] + gcol[(lane + 32) * P::SPITCH]);
     }
     __syncthreads();  // the stage (X1) is rewritten by the next matrix
   }
