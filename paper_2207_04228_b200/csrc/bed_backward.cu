@@ -23,11 +23,11 @@ static cudaError_t go_bwd_n(const BwdArgs& a) {
   return a.n == NMAX ? go_bwd<NMAX, true>(a) : go_bwd<NMAX, false>(a);
 }
 
-// 33 <= n <= 64 on the tensor cores (bed_backward_tc.cuh); BED_BWD_TC=0
-// selects the FFMA2 kernel instead (A/B comparisons)
+// 33 <= n <= 64 on the tensor cores (bed_backward_tc.cuh); BED_TC=0 selects
+// the FFMA2 kernel instead (A/B comparisons)
 static bool bwd_tc_enabled() {
   static const bool on = [] {
-    const char* e = getenv("BED_BWD_TC");
+    const char* e = getenv("BED_TC");
     return !(e && e[0] == '0');
   }();
   return on;

@@ -15,6 +15,9 @@
 // (status 4 = NonPositiveSpectrum, solver.py:133-139) and writes zeros.
 #include "bed_backward.cuh"
 #include "bed_launch.h"
+#include "bed_power_tc.cuh"
+
+#include <stdlib.h>
 
 namespace bed {
 
@@ -124,7 +127,31 @@ static cudaError_t go_pow_n(const PowArgs& a) {
   return a.n == NMAX ? go_pow<NMAX, true>(a) : go_pow<NMAX, false>(a);
 }
 
+// 33 <= n <= 64 on the tensor cores (bed_power_tc.cuh); BED_TC=0 selects the
+// FFMA2 kernel
+static bool pow_tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BED_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static cudaError_t go_pow_tc(const PowArgs& a) {
+  auto kern = bed_power_tc_kernel;
+  if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), PowTcParams::BYTES); e != cudaSuccess)
+    return e;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t slots = (int64_t)PowTcParams::CTAS_PER_SM * sms;
+  const unsigned grid = (unsigned)(a.batch < slots ? a.batch : slots);
+  kern<<<grid, PowTcParams::THREADS, PowTcParams::BYTES, a.stream>>>(
+      a.V, a.lam, a.out, a.status, a.flags, a.batch, a.n, a.p, a.floor_abs, a.needs_positive, a.merge);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_power(const PowArgs& a) {
+  if (a.n > 32 && pow_tc_enabled()) return go_pow_tc(a);
   if (a.n <= 4) return go_pow_n<4>(a);
   if (a.n <= 8) return go_pow_n<8>(a);
   if (a.n <= 16) return go_pow_n<16>(a);

@@ -1,6 +1,6 @@
 """Tensor-core backward (bed_backward_tc.cuh) against the float64 oracle and
 the FFMA2 kernel: relative gradient error per matrix, then device time at C5
-(dev tool, GPU).  BED_BWD_TC=0 runs the FFMA2 kernel for comparison."""
+(dev tool, GPU).  BED_TC=0 runs the FFMA2 kernel for comparison."""
 import os
 import sys
 
@@ -43,5 +43,5 @@ for _ in range(20):
     f()
 e.record()
 torch.cuda.synchronize()
-print(f"C5 backward n=64 b=8192 ({'tensor cores' if os.environ.get('BED_BWD_TC', '1') != '0' else 'FFMA2'}): "
+print(f"C5 backward n=64 b=8192 ({'tensor cores' if os.environ.get('BED_TC', '1') != '0' else 'FFMA2'}): "
       f"{s.elapsed_time(e) / 20 * 1e3:.1f} us", flush=True)

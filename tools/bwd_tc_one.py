@@ -1,5 +1,5 @@
 """One C5-sized Taylor backward launch (n = 64, 8192 matrices) for ncu
-captures of bed_backward_tc_kernel / bed_backward_kernel (BED_BWD_TC=0)."""
+captures of bed_backward_tc_kernel / bed_backward_kernel (BED_TC=0)."""
 import sys
 
 import torch

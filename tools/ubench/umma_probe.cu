@@ -8,7 +8,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <vector>
-#include "bed_backward_tc.cuh"
+#include "bed_tc.cuh"
 
 using namespace bed;
 
