@@ -325,8 +325,9 @@ def test_scatter_power_matches_float64(bed, n, m, p):
     ref = (q * w[:, None, :] ** p) @ q.transpose(0, 2, 1)
     err = np.linalg.norm(got.astype(np.float64) - ref, axis=(1, 2)) / np.linalg.norm(ref, axis=(1, 2))
     cond = w[:, -1] / w[:, 0]
-    # FP32: input rounding of S amplified by the condition number (to the |p|-ish power)
-    assert (err / (1.0 + cond) ** max(abs(p), 0.5)).max() <= 2e-6, (err.max(), cond.max())
+    # FP32 (3xTF32 products for n > 32): input rounding of S amplified by the
+    # condition number (to the |p|-ish power)
+    assert (err / (1.0 + cond) ** max(abs(p), 0.5)).max() <= 5e-6, (err.max(), cond.max())
     np.testing.assert_array_equal(got, got.transpose(0, 2, 1))
 
 
