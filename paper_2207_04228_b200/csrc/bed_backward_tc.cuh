@@ -4,9 +4,9 @@
 //   gA = sym( V (F o (V^T gV) + diag(gL)) V^T )      (bed_backward.cuh)
 //
 // Why 3xTF32: a single TF32 pass gives gradients 5-10e-4 off float64 (the gate
-// is 1e-4); splitting every operand x = hi + lo (hi = x with the low 13
-// mantissa bits cleared, lo = x - hi, exact) and accumulating hi*hi + hi*lo +
-// lo*hi in FP32 gives <= 1e-6 (profiles/r02_tf32_accuracy.txt).
+// is 1e-4); splitting every operand x = hi + lo (hi = x rounded to TF32,
+// lo = x - hi rounded to TF32, bed_tc.cuh) and accumulating lo*hi + hi*lo +
+// hi*hi gives ~1e-6 (tools/bwd_tc_check.py).
 //
 // A CTA (8 warps, two per SM) works on one matrix at a time, persistent over
 // the batch, with 64 x 64 x 8 MMAs (cta_group::1, M = 64: row m of D sits in
@@ -181,13 +181,13 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
       float x;
       x = tf32_hi(p_g[u]);
       *reinterpret_cast<float*>(buf(0, 0) + o) = x;
-      *reinterpret_cast<float*>(buf(0, 1) + o) = p_g[u] - x;
+      *reinterpret_cast<float*>(buf(0, 1) + o) = tf32_hi(p_g[u] - x);
       x = tf32_hi(p_kr[u]);
       *reinterpret_cast<float*>(buf(1, 0) + o) = x;
-      *reinterpret_cast<float*>(buf(1, 1) + o) = p_kr[u] - x;
+      *reinterpret_cast<float*>(buf(1, 1) + o) = tf32_hi(p_kr[u] - x);
       x = tf32_hi(p_rk[u]);
       *reinterpret_cast<float*>(buf(2, 0) + o) = x;
-      *reinterpret_cast<float*>(buf(2, 1) + o) = p_rk[u] - x;
+      *reinterpret_cast<float*>(buf(2, 1) + o) = tf32_hi(p_rk[u] - x);
     }
     bool pos = true;
     if (tid < 64) {

@@ -127,11 +127,13 @@ __global__ void __launch_bounds__(PowTcParams::THREADS, PowTcParams::CTAS_PER_SM
       const float4 v = pv[u];
       const float4 bh = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
       *reinterpret_cast<float4*>(b_hi + o) = bh;
-      *reinterpret_cast<float4*>(b_lo + o) = make_float4(v.x - bh.x, v.y - bh.y, v.z - bh.z, v.w - bh.w);
+      *reinterpret_cast<float4*>(b_lo + o) = make_float4(tf32_hi(v.x - bh.x), tf32_hi(v.y - bh.y), tf32_hi(v.z - bh.z),
+                                                          tf32_hi(v.w - bh.w));
       const float4 a = make_float4(v.x * sF[k0], v.y * sF[k0 + 1], v.z * sF[k0 + 2], v.w * sF[k0 + 3]);
       const float4 ah = make_float4(tf32_hi(a.x), tf32_hi(a.y), tf32_hi(a.z), tf32_hi(a.w));
       *reinterpret_cast<float4*>(a_hi + o) = ah;
-      *reinterpret_cast<float4*>(a_lo + o) = make_float4(a.x - ah.x, a.y - ah.y, a.z - ah.z, a.w - ah.w);
+      *reinterpret_cast<float4*>(a_lo + o) = make_float4(tf32_hi(a.x - ah.x), tf32_hi(a.y - ah.y), tf32_hi(a.z - ah.z),
+                                                          tf32_hi(a.w - ah.w));
     }
     proxy_fence_smem();
     tc_fence_before();

@@ -14,6 +14,9 @@
 #include "bed_backward.cuh"
 #include "bed_launch.h"
 #include "bed_scatter_regs.cuh"
+#include "bed_scatter_tc.cuh"
+
+#include <stdlib.h>
 
 namespace bed {
 
@@ -163,7 +166,30 @@ static cudaError_t go_scatter_small(const ScatArgs& a) {
   return cudaGetLastError();
 }
 
+// 33 <= n <= 64 on the tensor cores (bed_scatter_tc.cuh); BED_TC=0 selects
+// the FFMA2 kernel
+static bool scat_tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BED_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static cudaError_t go_scatter_tc(const ScatArgs& a) {
+  auto kern = bed_scatter_tc_kernel;
+  if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), ScatTcParams::BYTES); e != cudaSuccess)
+    return e;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t slots = (int64_t)ScatTcParams::CTAS_PER_SM * sms;
+  const unsigned grid = (unsigned)(a.batch < slots ? a.batch : slots);
+  kern<<<grid, ScatTcParams::THREADS, ScatTcParams::BYTES, a.stream>>>(a.X, a.out, a.batch, a.n, a.m, a.eps);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(const ScatArgs& a) {
+  if (a.n > 32 && scat_tc_enabled()) return go_scatter_tc(a);
   switch (a.n) {  // n <= 8: one thread per matrix (bed_scatter_regs.cuh)
     case 1: return go_scatter_small<1>(a);
     case 2: return go_scatter_small<2>(a);

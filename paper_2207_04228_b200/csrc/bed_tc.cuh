@@ -15,8 +15,13 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int k) {
   return (uint32_t)((row >> 3) * 2048 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
+// x rounded to TF32 (10 explicit mantissa bits, to nearest).  The 3xTF32 split
+// x = hi + lo uses it for both parts: hi = tf32(x), lo = tf32(x - hi), so the
+// tensor core reads both exactly and what is dropped (|.| <= 2^-22 |x|) has no
+// bias -- truncation would bias every product the same way, which adds up over
+// long sums (the covariance producer's sample axis).
 __device__ __forceinline__ float tf32_hi(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 // shared-memory matrix descriptor, version 1 (sm_100), no swizzle, K-major:
@@ -76,7 +81,8 @@ __device__ __forceinline__ void store8(uint8_t* hi, uint8_t* lo, int row, int k0
     xh.y = tf32_hi(d[4 * q + 1]);
     xh.z = tf32_hi(d[4 * q + 2]);
     xh.w = tf32_hi(d[4 * q + 3]);
-    xl = make_float4(d[4 * q] - xh.x, d[4 * q + 1] - xh.y, d[4 * q + 2] - xh.z, d[4 * q + 3] - xh.w);
+    xl = make_float4(tf32_hi(d[4 * q] - xh.x), tf32_hi(d[4 * q + 1] - xh.y), tf32_hi(d[4 * q + 2] - xh.z),
+                     tf32_hi(d[4 * q + 3] - xh.w));
     const uint32_t o = kmaj_off(row, k0 + 4 * q);
     *reinterpret_cast<float4*>(hi + o) = xh;
     *reinterpret_cast<float4*>(lo + o) = xl;
