@@ -12,7 +12,7 @@ for n in 16 24 32 64; do
   bash tools/ncu_export.sh ft$n "bed_fold_tma_kernel" 0 python tools/profile_cases.py $n
 done
 bash tools/ncu_export.sh bwd16 "bed_backward_kernel" 0 python tools/profile_cases.py 16
-bash tools/ncu_export.sh bwd64 "bed_backward_kernel" 0 python tools/profile_cases.py 64
+bash tools/ncu_export.sh bwd64 "bed_backward_tc_kernel" 0 python tools/profile_cases.py 64
 bash tools/ncu_export.sh pow16 "bed_power_kernel" 0 python tools/profile_cases.py 16 pow
 bash tools/ncu_export.sh scat16 "bed_scatter_kernel" 0 python tools/profile_cases.py scat
 bash tools/ncu_export.sh powf4 "bed_small_kernel" 0 python tools/profile_cases.py 4 powf
