@@ -29,5 +29,14 @@ bed.batched_eig(a, cfg)
 # chunked host path and a batch above the medium path's sub-warp tails
 x = oracle.gen_spd(3000, 4, 1).astype(np.float32)
 bed.batched_eig(x, bed.SolverConfig(deflation_tol=3e-12))
+# float64 host entry (host-thread validation, one stream per staging slot)
+bed.batched_eig(oracle.gen_spd(2100, 6, 3), bed.SolverConfig(deflation_tol=3e-12, max_double_steps=24))
+bed.batched_eig(oracle.gen_spd(70, 36, 3), bed.SolverConfig(deflation_tol=3e-12, max_double_steps=144))
+# fused power and covariance paths (one kernel for n <= 8), ragged m
+for n, m in ((3, 7), (4, 16), (8, 33), (12, 48), (40, 130), (64, 65)):
+    xs = torch.randn(67, n, m, device="cuda")
+    bed.scatter_power(xs, -0.5, 1e-2, check=False)
+    bed.scatter_eig(xs, 1e-2, check=False)
+    bed.power_of(bed.scatter_matrices(xs, 1e-2), 0.5, check=False)
 torch.cuda.synchronize()
 print("sanitize cases done")
