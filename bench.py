@@ -434,6 +434,11 @@ def torch_eigh_ms(torch, a, reps=3):
         for lo in range(0, a.shape[0], chunk):
             torch.linalg.eigh(a[lo:lo + chunk])
 
+    try:  # cuSOLVER handle creation and workspace queries happen on the first call
+        torch.linalg.eigh(a[: min(a.shape[0], 64)])
+        torch.cuda.synchronize()
+    except Exception:  # noqa: BLE001
+        pass
     for chunked in (0, 1 << 14, 1 << 12):
         try:
             best = float("inf")
