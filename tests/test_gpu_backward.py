@@ -141,3 +141,56 @@ def test_backward_outside_taylor_domain(bed):
     lam_t, v_t = bed.eigh(at, bed.SolverConfig(deflation_tol=3e-12), check=True)
     with pytest.raises(bed.NonPositiveSpectrum):
         (v_t * gv).sum().backward()
+
+
+# ---- the tcgen05 tier (33 <= n <= 64, bed_backward_tc.cuh): ragged n and
+# batches, null cotangents, the domain rule and the large-degree limit
+
+
+@pytest.mark.parametrize("n,b", [(33, 1), (47, 5), (57, 333), (64, 2)])
+def test_tensor_core_backward_ragged(bed, n, b):
+    rng = np.random.default_rng(n + b)
+    q, _ = np.linalg.qr(rng.standard_normal((b, n, n)))
+    lam = np.sort(rng.uniform(0.1, 4.0, (b, n)), axis=1)[:, ::-1].copy()
+    v = q.astype(np.float32)
+    vt, lt = torch.from_numpy(v).cuda(), torch.from_numpy(lam.astype(np.float32)).cuda()
+    gv = rng.standard_normal((b, n, n)).astype(np.float32)
+    gl = rng.standard_normal((b, n)).astype(np.float32)
+    for g_v, g_l in ((gv, gl), (None, gl), (gv, None)):
+        ga = bed.taylor_backward(vt, lt, None if g_v is None else torch.from_numpy(g_v).cuda(),
+                                 None if g_l is None else torch.from_numpy(g_l).cuda()).cpu().numpy()
+        ref = oracle.taylor_backward(v.astype(np.float64), lam.astype(np.float32).astype(np.float64), g_v, g_l)
+        assert P.grad_err(ga, ref).max() <= P.GRAD_TOL
+        np.testing.assert_array_equal(ga, ga.transpose(0, 2, 1))
+
+
+def test_tensor_core_backward_domain_and_degree(bed):
+    n, b = 40, 24
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((b, n, n)))
+    lam = np.sort(rng.uniform(-2.0, 3.0, (b, n)), axis=1)[:, ::-1].copy()
+    lam[:8] = np.abs(lam[:8]) + 0.5  # SPD rows
+    vt = torch.from_numpy(q.astype(np.float32)).cuda()
+    lt = torch.from_numpy(lam.astype(np.float32)).cuda()
+    gv = torch.from_numpy(rng.standard_normal((b, n, n)).astype(np.float32)).cuda()
+    ga = bed.taylor_backward(vt, lt, gv, None).cpu().numpy()
+    ref = oracle.taylor_backward(vt.cpu().numpy(), lt.cpu().numpy(), gv.cpu().numpy(), None)
+    assert P.grad_err(ga, ref).max() <= P.GRAD_TOL
+    inside = oracle.taylor_domain(lt.cpu().numpy())
+    with pytest.raises(bed.NonPositiveSpectrum) as err:
+        bed.taylor_backward(vt, lt, gv, None, check=True)
+    assert err.value.batch_index == int(np.nonzero(~inside)[0][0])
+    # large degree on a geometric SPD spectrum (neighbour ratio 0.9: 0.9^300 ~ 2e-14)
+    # -> the exact 1/(l_j - l_i)
+    lg = np.tile(3.0 * 0.9 ** np.arange(n), (8, 1))
+    spd = torch.from_numpy(lg.astype(np.float32)).cuda()
+    v8 = vt[:8].contiguous()
+    g300 = bed.taylor_backward(v8, spd, gv[:8].contiguous(), None, 300).cpu().numpy()
+    l64 = spd.cpu().numpy().astype(np.float64)
+    vv = v8.cpu().numpy().astype(np.float64)
+    diff = l64[:, None, :] - l64[:, :, None]
+    fexact = np.where(np.eye(n, dtype=bool), 0.0, 1.0 / np.where(np.eye(n, dtype=bool), 1.0, diff))
+    m = vv.transpose(0, 2, 1) @ gv[:8].cpu().numpy().astype(np.float64)
+    gex = vv @ (fexact * m) @ vv.transpose(0, 2, 1)
+    gex = (gex + gex.transpose(0, 2, 1)) / 2
+    assert P.grad_err(g300, gex).max() <= 1e-3
