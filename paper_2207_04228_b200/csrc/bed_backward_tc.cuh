@@ -8,21 +8,23 @@
 // lo = x - hi rounded to TF32, bed_tc.cuh) and accumulating lo*hi + hi*lo +
 // hi*hi gives ~1e-6 (tools/bwd_tc_check.py).
 //
-// A CTA (8 warps, two per SM) works on one matrix at a time, persistent over
+// A CTA (8 warps, three per SM) works on one matrix at a time, persistent over
 // the batch, with 64 x 64 x 8 MMAs (cta_group::1, M = 64: row m of D sits in
 // TMEM lane 32 (m / 16) + m % 16).  The three products are arranged so every
 // intermediate leaves the epilogue in the row-per-thread orientation the next
 // product reads:
 //   P1  D = gV^T V   = M^T      A = gV^T, B = V^T (staged transposed from HBM)
 //   E1  M'^T = (F o M + diag gL)^T, row by row            -> X1 (B of P2)
-//   P2  D = V M'     = W        A = V (staged as is),  B = M'^T
-//   E2  W, row by row                                      -> X2 (A of P3)
+//   P2  D = V M'     = W        A = V (staged as is, in X2),  B = M'^T
+//   E2  W, row by row                                      -> X1 (A of P3)
 //   P3  D = W V^T    = G        A = W, B = V
 //   E3  G through a padded shared stage, gA = (G + G^T) / 2, coalesced
 // Operands live in shared memory in the canonical K-major no-swizzle layout
 // (8-row x 16-byte core matrices; LBO = 128 B between the two core matrices
 // of one K = 8 step, SBO = 2 KB between 8-row groups), each as hi and lo
-// copies: 3 operands x 2 x 16 KB, two CTAs per SM.  One elected thread issues the 3 x 8 MMAs of
+// copies in two operand buffers (2 x 2 x 16 KB): X1 = gV^T -> M'^T -> W -> the
+// G stage, X2 = V^T -> V (V's 128-bit loads are issued with P1, stored after
+// E1, once P1 has read V^T), so three CTAs fit per SM.  One elected thread issues the 3 x 8 MMAs of
 // a product and commits them to an mbarrier the CTA waits on.
 #pragma once
 
@@ -36,13 +38,13 @@ namespace bed {
 struct BwdTcParams {
   static constexpr int THREADS = 256;  // 8 warps: warps w and w + 4 share TMEM lanes, split columns
   static constexpr int BUF = 64 * 64 * 4;              // one operand copy (hi or lo), bytes
-  static constexpr int OPS = 3;                        // X1 (gV^T -> M'^T -> G stage), X2 (V^T -> W), X3 (V)
+  static constexpr int OPS = 2;                        // X1 (gV^T -> M'^T -> W -> G stage), X2 (V^T -> V)
   static constexpr int OFF_LAM = OPS * 2 * BUF;        // lam[64], inv[64], gL[64]
   static constexpr int OFF_BAR = OFF_LAM + 3 * 64 * 4;
   static constexpr int OFF_TMEM = OFF_BAR + 8;
   static constexpr int OFF_OUT = OFF_TMEM + 8;
   static constexpr size_t BYTES = OFF_OUT + 16;
-  static constexpr int CTAS_PER_SM = 2;
+  static constexpr int CTAS_PER_SM = 3;
   static constexpr int SPITCH = 65;                    // G stage row pitch (floats)
   static_assert(64 * SPITCH * 4 <= 2 * BUF, "G stage fits in X1");
 };
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
   // matrix's loads are issued while this one's last product runs (prefetch),
   // its stores at the top of the next iteration (stage).
   constexpr int kStageU = 16;  // 128 core blocks / 8 warps
-  float p_rk[kStageU], p_kr[kStageU], p_g[kStageU], p_l = 0.0f, p_gl = 0.0f;
+  float p_kr[kStageU], p_g[kStageU], p_l = 0.0f, p_gl = 0.0f;
   auto prefetch = [&](int64_t mm) {
     const bool have = mm < batch;
     const float* vb = V + (have ? mm : 0) * nn;
@@ -164,7 +166,6 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
       const int c = warp + 8 * u;
       const int row = 8 * (c >> 4) + (lane >> 2), k = 4 * (c & 15) + (lane & 3);
       const bool ok = have && row < n && k < n;
-      p_rk[u] = ok ? __ldg(vb + row * n + k) : 0.0f;  // V[row][k]
       p_kr[u] = ok ? __ldg(vb + k * n + row) : 0.0f;  // V[k][row]
       p_g[u] = (ok && gb) ? __ldg(gb + k * n + row) : 0.0f;
     }
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
     p_l = okl ? __ldg(lam + mm * n + tid) : 0.0f;
     p_gl = (okl && gL) ? __ldg(gL + mm * n + tid) : 0.0f;
   };
+  const bool vec4 = (n % 4 == 0) && (reinterpret_cast<uintptr_t>(V) & 15) == 0;
   prefetch(blockIdx.x);
   for (int64_t m = blockIdx.x; m < batch; m += gridDim.x) {
 #pragma unroll
@@ -185,9 +187,6 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
       x = tf32_hi(p_kr[u]);
       *reinterpret_cast<float*>(buf(1, 0) + o) = x;
       *reinterpret_cast<float*>(buf(1, 1) + o) = tf32_hi(p_kr[u] - x);
-      x = tf32_hi(p_rk[u]);
-      *reinterpret_cast<float*>(buf(2, 0) + o) = x;
-      *reinterpret_cast<float*>(buf(2, 1) + o) = tf32_hi(p_rk[u] - x);
     }
     bool pos = true;
     if (tid < 64) {
@@ -205,6 +204,29 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
 
     // ---- P1: D = gV^T V = M^T;  E1: M'^T[r][c] = F(c, r) M[c][r] + (c == r) gL[r] -> X1
     issue(0, 1);
+    // V as stored (the A of P2, the B of P3) goes into X2 once P1 has read V^T
+    // from it: its 128-bit loads are issued now, the stores after E1
+    float4 vr[4];
+    {
+      const float* vb = V + m * nn;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = warp + 8 * u;  // 32 core-block steps: 8 rows x 4 k-groups each
+        const int row = 8 * (c >> 2) + (lane & 7), k0 = 4 * (4 * (c & 3) + (lane >> 3));
+        vr[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (row < n && k0 < n) {
+          const float* src = vb + row * n + k0;
+          if (vec4) {
+            vr[u] = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            vr[u].x = __ldg(src);
+            vr[u].y = k0 + 1 < n ? __ldg(src + 1) : 0.0f;
+            vr[u].z = k0 + 2 < n ? __ldg(src + 2) : 0.0f;
+            vr[u].w = k0 + 3 < n ? __ldg(src + 3) : 0.0f;
+          }
+        }
+      }
+    }
     wait_mma();
     {
       bool off = false;
@@ -228,9 +250,20 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
       }
       if (off) atomicOr(&outside[0], 1);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = warp + 8 * u;
+      const int row = 8 * (c >> 2) + (lane & 7), k0 = 4 * (4 * (c & 3) + (lane >> 3));
+      const float4 v = vr[u];
+      const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+      const uint32_t o = kmaj_off(row, k0);
+      *reinterpret_cast<float4*>(buf(1, 0) + o) = h;
+      *reinterpret_cast<float4*>(buf(1, 1) + o) =
+          make_float4(tf32_hi(v.x - h.x), tf32_hi(v.y - h.y), tf32_hi(v.z - h.z), tf32_hi(v.w - h.w));
+    }
     sync_for_mma();
-    // ---- P2: D = V M' = W;  E2: W -> X2 (A of P3)
-    issue(2, 0);
+    // ---- P2: D = V M' = W;  E2: W -> X1 (A of P3; P2 has read M'^T)
+    issue(1, 0);
     wait_mma();
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
@@ -238,11 +271,11 @@ __global__ void __launch_bounds__(BwdTcParams::THREADS, BwdTcParams::CTAS_PER_SM
       tmem_ld16(trow + 16u * q, d);
       tmem_wait_ld();
       split_half(d, lane, e);
-      store8(buf(1, 0), buf(1, 1), r, c_lo + 16 * q + c_half, e);
+      store8(buf(0, 0), buf(0, 1), r, c_lo + 16 * q + c_half, e);
     }
     sync_for_mma();
-    // ---- P3: D = W V^T = G;  E3: G through the X1 region (free since P2)
-    issue(1, 2);
+    // ---- P3: D = W V^T = G;  E3: G through the X1 region (P3 has read W)
+    issue(0, 1);
     prefetch(m + gridDim.x);  // in flight during P3, E3 and the stores
     wait_mma();
     float* sg = reinterpret_cast<float*>(buf(0, 0));
