@@ -241,12 +241,14 @@ def time_steps(torch, step, k, w, dist=None):
     return sec
 
 
-def cpu_oracle_rate(n, sample, threads, mode="fwd"):
+def cpu_oracle_rate(n, sample, threads, mode="fwd", a=None):
     """Matrices/s of the reference algorithm's C restatement (oracle/) on
-    host cores: per-matrix gating, same tolerance/budget as the GPU run."""
+    host cores: per-matrix gating, same tolerance/budget as the GPU run.
+    `a`: the inputs, generated here when not given (generation is untimed)."""
     import oracle
 
-    a = oracle.gen_spd(sample, n, 12345)
+    if a is None:
+        a = oracle.gen_spd(sample, n, 12345)
     t0 = time.perf_counter()
     r = oracle.forward(a, deflation_tol=TOL, max_double_steps=4 * n, gate=oracle.GATE_MATRIX,
                        threads=threads, chunk=max(64, sample // (8 * threads)))
@@ -385,26 +387,42 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     if rank == 0:
+        t0 = time.perf_counter()
+
+        def lap(what):  # wall time of each section, on stderr (the JSON line stays on stdout)
+            nonlocal t0
+            t1 = time.perf_counter()
+            print(f"[bench] {what}: {t1 - t0:.1f} s", file=sys.stderr, flush=True)
+            t0 = t1
+
         line["e2e"] = e2e_host(torch, bed, n, batch, max(3, min(args.steps, 10)), local)
+        lap("e2e (C ABI host path)")
         line["e2e_numpy_api"] = e2e_numpy_api(bed, n, batch, 3)
+        lap("e2e (float64 numpy API)")
         if not args.quick:
             line["other_configs"] = other_configs(torch, bed, dev, hbm_peak)
+            lap("other_configs")
         threads = os.cpu_count() or 1
         # a bounded sample (~10 s of host work): repeated solves of one batch
         # of up to 2^20 matrices, so memory stays small
         sample = calibrated_sample(n, threads, 3.0, 1 << 20)
+        import oracle
+
+        a_cpu = oracle.gen_spd(sample, n, 12345)  # generated once, solved repeatedly
         total, secs, reps = 0, 0.0, 0
         while secs < 10.0 and reps < 1000:
-            _, dt = cpu_oracle_rate(n, sample, threads)
+            _, dt = cpu_oracle_rate(n, sample, threads, a=a_cpu)
             total += sample
             secs += dt
             reps += 1
         rate = total / secs
+        lap("cpu_baseline")
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"{reps} x {sample} 4x4 matrices (same distribution), oracle/ "
                                           "C restatement of the reference solver, per-matrix gate, "
                                           f"tol {TOL:g}, budget 16, {threads} threads, {secs:.1f} s"}
         te = torch_eigh_ms(torch, step.a)
+        lap("torch.linalg.eigh baseline")
         line["torch_eigh_baseline"] = (
             {"value": batch / (te * 1e-3), "unit": UNIT, "batch": batch, "ms": te,
              "what": "torch.linalg.eigh fp32 on the same resident batch, 1 B200, CUDA events"}
@@ -414,6 +432,7 @@ def run_ours(args):
                 line["reference_numba"] = reference_numba(n)
             except Exception as exc:  # noqa: BLE001
                 line["reference_numba"] = {"unavailable": str(exc)[:160]}
+            lap("reference_numba")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -439,7 +458,8 @@ def torch_eigh_ms(torch, a, reps=3):
         torch.cuda.synchronize()
     except Exception:  # noqa: BLE001
         pass
-    for chunked in (0, 1 << 14, 1 << 12):
+    # cusolverDnXsyevBatched rejects whole batches of 32768 and up: go straight to chunks
+    for chunked in ((0,) if a.shape[0] < 32768 else ()) + (1 << 14, 1 << 12):
         try:
             best = float("inf")
             for r in range(reps + 1):
@@ -476,6 +496,7 @@ def other_configs(torch, bed, dev, hbm_peak):
              (4, 1 << 22, "fwdpow"), (4, 1 << 22, "powf"), (16, 65536, "powf"),
              (4, 1 << 20, "scatpow"), (8, 1 << 18, "scatpow"), (16, 65536, "scatpow")]
     for n, b, mode in cases:
+        t_row = time.perf_counter()
         st = Step(torch, bed, n, b, mode, dev, seed=n)
         reps = 50 if b <= 4096 else 10
         # best of three timed blocks after warm-up: the first calls at a new
@@ -494,6 +515,7 @@ def other_configs(torch, bed, dev, hbm_peak):
             row["torch_eigh_ms"] = te
             row["speedup_vs_torch_eigh"] = (te / (sec * 1e3)) if te else None
         rows.append(row)
+        print(f"[bench]   row n={n} b={b} {mode}: {time.perf_counter() - t_row:.1f} s", file=sys.stderr, flush=True)
         del st
         torch.cuda.empty_cache()
     return rows
@@ -574,9 +596,12 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     budget = 60.0 / max(1, args.steps + args.warmup)
     sample = calibrated_sample(n, threads, budget, HEADLINE["batch"])
+    import oracle
+
+    a = oracle.gen_spd(sample, n, 12345)  # generated once (untimed), solved every step
     for _ in range(args.warmup):
-        cpu_oracle_rate(n, sample, threads)
-    secs = [cpu_oracle_rate(n, sample, threads)[1] for _ in range(args.steps)]
+        cpu_oracle_rate(n, sample, threads, a=a)
+    secs = [cpu_oracle_rate(n, sample, threads, a=a)[1] for _ in range(args.steps)]
     sec = statistics.median(secs)
     value = sample / sec
     line = {
