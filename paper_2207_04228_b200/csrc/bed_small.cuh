@@ -45,6 +45,7 @@
 namespace bed {
 
 constexpr int kSmallThreads = 128;
+
 // largest n whose QR loop sweeps every position unmasked (small_sweep_full)
 constexpr int kUnmaskedMaxN = 4;  // n = 8 measured equal either way
 
@@ -220,8 +221,14 @@ __device__ __forceinline__ int small_deflate_zero(float (&e)[N], int m, float ep
 // covariance producer of SURVEY.md 8(f) row 3) in registers, in one pass
 // shifted by each channel's first sample (as bed_scatter.cu), instead of
 // reading A: the covariance never reaches memory.
+// CTAs per SM the register allocation must allow: n = 5, 6 fit six (85
+// registers) and n = 7 five (102) without spilling in the QR loop; n = 8 keeps
+// its 125 (capped at 102 it spills inside the loop: 0.41 vs 0.32 ms at 1 M)
+template <int N>
+constexpr int small_min_blocks() { return (N == 5 || N == 6) ? 6 : (N == 7 ? 5 : 1); }
+
 template <int N, bool VECS, bool POW = false, bool SCAT = false>
-__global__ void __launch_bounds__(kSmallThreads)
+__global__ void __launch_bounds__(kSmallThreads, small_min_blocks<N>())
     bed_small_kernel(const float* __restrict__ A, int64_t batch, float* __restrict__ evals,
                      float* __restrict__ evecs, int32_t* __restrict__ status_out,
                      int32_t* __restrict__ steps_out, int32_t* __restrict__ flags, KernelCfg cfg,
