@@ -302,9 +302,11 @@ def e2e_numpy_api(bed, n, batch, steps):
     (solver.py:79-112) -> bed_forward_host_f64: float64 validation +
     symmetrisation and the FP32 cast on host threads into page-locked staging,
     H2D, solve, D2H, float64 results -- all timed, chunks overlapped."""
-    import oracle
+    from paper_2207_04228_b200.datagen import gen_spd_device
 
-    a = oracle.gen_spd(min(batch, 1 << 20), n, 7)
+    # the same distribution, generated by the package (oracle/ stays the
+    # checker); float64 on the host, as a reference user holds it
+    a = gen_spd_device(min(batch, 1 << 20), n, 7).double().cpu().numpy()
     cfg = bed.SolverConfig(deflation_tol=TOL, max_double_steps=4 * n)
     bed.batched_eig(bed.BatchedSymmetric(a), cfg)
     times = []
