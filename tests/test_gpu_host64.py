@@ -127,3 +127,34 @@ def test_host_f64_no_convergence_payload(bed):
                         bed.SolverConfig(deflation_tol=3e-12, max_double_steps=1,
                                          strict_convergence=False))
     assert r.eigenvalues.shape == (b, n)
+
+
+def test_integration_stub_runs_as_documented(bed):
+    """The ctypes stub of INTEGRATION.md section 2, run verbatim against this
+    library: the same results and errors as batched_eig on float64 numpy."""
+    import ctypes
+    import os
+    import re
+
+    from paper_2207_04228_b200 import _native, core
+
+    src = open(os.path.join(os.path.dirname(__file__), "..", "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# batchedeig/_b200\.py.*?)```", src, re.S).group(1)
+    code = code.replace("from .core import NoConvergence, NonFinite, NonSymmetric\n", "")
+    code = code.replace('ctypes.CDLL("libbed200.so")', "ctypes.CDLL(LIB)")
+    ns = {"NoConvergence": core.NoConvergence, "NonFinite": core.NonFinite,
+          "NonSymmetric": core.NonSymmetric, "LIB": _native.LIB_PATH, "ctypes": ctypes}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    stub = ns["batched_eig_b200"]
+    n, b = 12, 500
+    a = oracle.gen_spd(b, n, 4)
+    cfg = bed.SolverConfig(max_double_steps=4 * n, **VERIFY)
+    lam, vec = stub(bed.BatchedSymmetric(a), cfg)
+    r = bed.batched_eig(bed.BatchedSymmetric(a), cfg)
+    np.testing.assert_array_equal(lam, r.eigenvalues)
+    np.testing.assert_array_equal(vec, r.eigenvectors)
+    bad = a.copy()
+    bad[7, 2, 3] = np.inf
+    with pytest.raises(bed.NonFinite) as err:
+        stub(bed.BatchedSymmetric(bad), cfg)
+    assert err.value.batch_index == 7 and err.value.position == (2, 3)
