@@ -221,11 +221,13 @@ __device__ __forceinline__ int small_deflate_zero(float (&e)[N], int m, float ep
 // covariance producer of SURVEY.md 8(f) row 3) in registers, in one pass
 // shifted by each channel's first sample (as bed_scatter.cu), instead of
 // reading A: the covariance never reaches memory.
-// CTAs per SM the register allocation must allow: n = 5, 6 fit six (85
-// registers) and n = 7 five (102) without spilling in the QR loop; n = 8 keeps
-// its 125 (capped at 102 it spills inside the loop: 0.41 vs 0.32 ms at 1 M)
+// CTAs per SM the register allocation must allow: 0 = no constraint (ptxas's
+// own choice -- an explicit 1 is NOT the same and gave the n = 4 kernel 80
+// registers instead of 54); n = 7 at five CTAs (102 registers, a 48-byte spill
+// outside the loop): 1 M matrices 0.298 -> 0.284 ms.  n = 5, 6 and 8 measured
+// best unconstrained (n = 8 capped at five spills inside the QR loop).
 template <int N>
-constexpr int small_min_blocks() { return (N == 5 || N == 6) ? 6 : (N == 7 ? 5 : 1); }
+constexpr int small_min_blocks() { return N == 7 ? 5 : 0; }
 
 template <int N, bool VECS, bool POW = false, bool SCAT = false>
 __global__ void __launch_bounds__(kSmallThreads, small_min_blocks<N>())
