@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <omp.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <mutex>
@@ -487,6 +488,17 @@ struct HostStage {
 
 HostStage g_stage[64];
 
+// Ask for transparent huge pages on a caller's freshly allocated result array:
+// its first touch happens in the output conversion, and with 4 KB pages the
+// page faults (one per 4 KB of float64 results) cost more than the conversion.
+// Advisory only; errors are ignored.
+void advise_huge(void* p, size_t bytes) {
+  constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+  const uintptr_t b = (reinterpret_cast<uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(kHuge - 1);
+  if (p && e > b) madvise(reinterpret_cast<void*>(b), e - b, MADV_HUGEPAGE);
+}
+
 int host_threads(int32_t req) {
   if (req > 0) return std::min(req, 256);
   const unsigned hw = std::thread::hardware_concurrency();
@@ -551,6 +563,8 @@ int bed_forward_host_f64(const double* A, int64_t batch, int32_t n, double* eval
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   const int nthr = host_threads(threads);
+  advise_huge(evals, sizeof(double) * (size_t)batch * n);
+  if (cfg->compute_vectors) advise_huge(evecs, sizeof(double) * (size_t)batch * n * n);
 
   const bool vecs = cfg->compute_vectors != 0;
   const int64_t nn = (int64_t)n * n;
