@@ -27,11 +27,21 @@
 // (householder.py:37-39) at FP32 resolution.
 #pragma once
 
+#include <type_traits>
+
 #include "bed_f32x2.cuh"
 #include "bed_split_ws.cuh"
 #include "bed_tile.cuh"
 
+#ifndef HH_GROUP_MIN
+#define HH_GROUP_MIN 32
+#endif
+
 namespace bed {
+
+// Householder steps as runtime loops over groups of four (bed_hh_kernel)
+template <int NMAX>
+constexpr bool kHHGroupSteps = NMAX >= HH_GROUP_MIN;
 
 template <int NMAX>
 struct HHParams {
@@ -202,14 +212,21 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
   // ---- Householder reduction; reflector i stored in st row i.  The step
   // loop is expanded by template recursion so every column index is a
   // compile-time constant (NVVM's unroller gives up on the n = 64 body).
-  static_for<0, NMAX - 2>([&](auto ic) {
-    constexpr int i = decltype(ic)::value;
-    if (!EXACT && i >= n - 2) return;
+  // One step for reflector i: K0 / K1 are the (compile-time) first column
+  // pairs of p = A u and of the update -- at most the step's own -- and the
+  // pivot column is picked among NC compile-time candidates from C0.
+  auto hh_step = [&](const int i, auto k0c, auto k1c, auto c0c, auto ncc) {
+    constexpr int K0 = decltype(k0c)::value, K1 = decltype(k1c)::value;
+    constexpr int C0 = decltype(c0c)::value, NC = decltype(ncc)::value;
     float x[R];
     float ss = 0.0f;
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      x[rr] = (l + L * rr > i) ? col_of<NP>(a[rr], i) : 0.0f;
+      float c = col_of<NP>(a[rr], C0);
+#pragma unroll
+      for (int q = 1; q < NC; ++q)
+        if (C0 + q < NMAX) c = (i == C0 + q) ? col_of<NP>(a[rr], C0 + q) : c;
+      x[rr] = (l + L * rr > i) ? c : 0.0f;
       ss = fmaf(x[rr], x[rr], ss);
     }
     ss = grp.sum(ss);
@@ -218,8 +235,11 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     if (ss > 0x1p-120f) {
       // sigma = sign(x_0) ||x||, u0 = x_0 + sigma, ||u||^2 = 2 sigma u0
       // (householder.py:97-118; the tail is already at unit scale)
-      constexpr int pr = (i + 1) / L, pl = (i + 1) % L;
-      const float pivot = grp.bcast(x[pr], pl);
+      const int pr = (i + 1) / L, pl = (i + 1) % L;
+      float xp = x[0];
+#pragma unroll
+      for (int rr = 1; rr < R; ++rr) xp = (rr == pr) ? x[rr] : xp;
+      const float pivot = grp.bcast(xp, pl);
       const float nrm = ss * rsqrt_nr(ss);
       const float sigma = pivot >= 0.0f ? nrm : -nrm;
       const float u0 = pivot + sigma;
@@ -231,7 +251,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       }
       grp.sync();
       // p = 2 A u (two accumulators per row for ILP), K = u^T p, q = p - K u
-      constexpr int k0 = ((i + 1) / 2) & ~1;  // 16-byte aligned start; u = 0 below i+1
+      constexpr int k0 = K0;  // 16-byte aligned start; u = 0 below i+1
       float p[R];
       float kk = 0.0f;
       {
@@ -263,7 +283,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       }
       grp.sync();
       // A <- A - q u^T - u q^T on columns >= i (u, q vanish on the rest)
-      constexpr int k1 = (i / 2) & ~1;
+      constexpr int k1 = K1;
 #pragma unroll
       for (int k = k1; k < NP; k += 2) {
         const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
@@ -283,7 +303,29 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         if (l + L * rr < NMAX) urow[l + L * rr] = 0.0f;
     }
     grp.sync();
-  });
+  };
+  if constexpr (kHHGroupSteps<NMAX>) {
+    // four steps per group in a runtime loop, their columns picked by selects:
+    // ~4x less code than one expanded body per step (the unrolled form leaves
+    // the SM 11-20 % of cycles without instructions at n >= 32)
+    static_for<0, (NMAX - 2 + 3) / 4>([&](auto gc) {
+      constexpr int g = decltype(gc)::value;
+#pragma unroll 1
+      for (int t = 0; t < 4; ++t) {
+        const int i = 4 * g + t;
+        if (i >= NMAX - 2 || (!EXACT && i >= n - 2)) break;
+        hh_step(i, std::integral_constant<int, 2 * g>{}, std::integral_constant<int, 2 * g>{},
+                std::integral_constant<int, 4 * g>{}, std::integral_constant<int, 4>{});
+      }
+    });
+  } else {
+    static_for<0, NMAX - 2>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if (!EXACT && i >= n - 2) return;
+      hh_step(i, std::integral_constant<int, ((i + 1) / 2) & ~1>{}, std::integral_constant<int, (i / 2) & ~1>{},
+              std::integral_constant<int, i>{}, std::integral_constant<int, 1>{});
+    });
+  }
 
   // ---- band: D[r] = a(r, r), E[r-1] = a(r, r-1), picked with compares on
   // the lane index so no register array is indexed at run time
@@ -313,11 +355,9 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         v[rr][k] = f2_make(l + L * rr == 2 * k ? 1.0f : 0.0f, l + L * rr == 2 * k + 1 ? 1.0f : 0.0f);
-    static_for<0, NMAX - 2>([&](auto ic) {
-      constexpr int i = decltype(ic)::value;
-      if (!EXACT && i >= n - 2) return;
+    auto p_step = [&](const int i, auto k0c) {
       const float* urow = st + i * SROW;
-      constexpr int k0 = ((i + 1) / 2) & ~1;
+      constexpr int k0 = decltype(k0c)::value;
       f2 acc0[R], acc1[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = f2_bc(0.0f);
@@ -345,7 +385,24 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
           if (k + 1 < NP) v[rr][k + 1] = ffma2(f2_bc(t[rr]), f2_make(u4.z, u4.w), v[rr][k + 1]);
         }
       }
-    });
+    };
+    if constexpr (kHHGroupSteps<NMAX>) {
+      static_for<0, (NMAX - 2 + 3) / 4>([&](auto gc) {
+        constexpr int g = decltype(gc)::value;
+#pragma unroll 1
+        for (int t = 0; t < 4; ++t) {
+          const int i = 4 * g + t;
+          if (i >= NMAX - 2 || (!EXACT && i >= n - 2)) break;
+          p_step(i, std::integral_constant<int, 2 * g>{});
+        }
+      });
+    } else {
+      static_for<0, NMAX - 2>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if (!EXACT && i >= n - 2) return;
+        p_step(i, std::integral_constant<int, ((i + 1) / 2) & ~1>{});
+      });
+    }
     grp.sync();  // every lane is done reading reflectors
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
