@@ -179,22 +179,23 @@ __global__ void __launch_bounds__(kQThreads)
     }
     float lo, hi;
     wilkinson_shifts(ta, tb, td, lo, hi);
-    const int ma = run ? m : 0;
-    const int mwa = __reduce_max_sync(0xffffffffu, ma);
-    qr_sweep<NMAX, VECS>(d, e, ma, hi, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr, mwa);
-    record_end(mwa, mwa, ma);
+    // the two sweeps of the double step (shifts hi, then lo) share one copy
+    // of the unrolled sweep code: a runtime loop of two halves the kernel's
+    // size (instruction-cache misses stalled it at n = 64)
     srs += run ? n - m : 0;
-    rot += run ? m - 1 : 0;
-    if (run) m = qr_deflate<NMAX>(e, m, cfg.eps);
-    const int mb = (run && m > 2) ? m : 0;
-    rot += mb > 2 ? mb - 1 : 0;
-    const int mwb = __reduce_max_sync(0xffffffffu, mb);
-    if (mwb > 2) {
-      qr_sweep<NMAX, VECS>(d, e, mb, lo, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr, mwb);
-      record_end(mwb, mwb, mb);
+    int mcur = run ? m : 0;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int mw = __reduce_max_sync(0xffffffffu, mcur);
+      if (h == 1 && mw <= 2) break;
+      rot += mcur > 2 ? mcur - 1 : 0;
+      qr_sweep<NMAX, VECS>(d, e, mcur, h ? lo : hi, VECS ? recw + (size_t)nrec * (NMAX - 1) * 32 : nullptr,
+                           mw);
+      record_end(mw, mw, mcur);
+      if (run) m = qr_deflate<NMAX>(e, m, cfg.eps);
+      mcur = (run && m > 2) ? m : 0;
     }
     if (run) {
-      m = qr_deflate<NMAX>(e, m, cfg.eps);
       ++steps;
       run = m > 2;
     }
