@@ -36,7 +36,7 @@ struct FTParams {
   static constexpr int MINB = NMAX <= 24 ? 4 : (NMAX <= 32 ? 2 : 1);
   static constexpr int NB = 6;
   static constexpr int NW = FT / 32;   // fold warps
-  static constexpr int BLK = kFoldBlk;  // positions per fold block (one branch, loads hoisted)
+  static constexpr int BLK = fold_blk<NMAX>();  // positions per fold block (one branch, loads hoisted)
   static constexpr int POS = NMAX - 1;
   static constexpr int SLOT = POS * 32;  // float2 per ring slot: a whole sweep record [position][lane]
   static constexpr int RING = NB * SLOT * 2;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
       for (int s = s0; s < min(nrec, s0 + 32); ++s) {
         const int b = s % NB;
         const int mw = __shfl_sync(0xffffffffu, mw_l, s - s0);
-        const int np = min(POS, (mw - 1 + kFoldBlk - 1) / kFoldBlk * kFoldBlk);
+        const int np = min(POS, (mw - 1 + P::BLK - 1) / P::BLK * P::BLK);
         if (s >= NB) mbar_wait(empty + b, ((s / NB) & 1) ^ 1);
         if (lane == s - s0) {
 #pragma unroll

@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kQThreads)
   // active size (the fold skips a lane's no-op sweeps and positions)
   auto record_end = [&](int mw, int written, int mine) {
     if constexpr (VECS) {
-      const int padded = min(NMAX - 1, ((mw - 1 + kFoldBlk - 1) / kFoldBlk) * kFoldBlk);
+      constexpr int kBlk = fold_blk<NMAX>();
+      const int padded = min(NMAX - 1, ((mw - 1 + kBlk - 1) / kBlk) * kBlk);
       pad(min(written, NMAX - 1), padded);
       if (lane == 0) mw_rec[nrec] = mw;
       ml_rec[(size_t)nrec * 32] = (uint8_t)mine;

@@ -7,8 +7,12 @@
 namespace bed {
 
 // positions per record block: Q pads each sweep's record with identities to
-// a whole block, F copies and applies whole blocks
-constexpr int kFoldBlk = 4;
+// a whole block, F copies and applies whole blocks (one branch per block).  8
+// at n = 64: fewer block joins, each of which costs the fold register moves
+// (forward 8 192 x 64^2: 1.224 -> 1.174 ms); 4 below, where the padding costs
+// more than the joins
+template <int NMAX>
+constexpr int fold_blk() { return NMAX >= 64 ? 8 : 4; }
 constexpr int kQThreads = 32;  // one warp per CTA: small batches (n = 64) still reach every SM
 
 struct SplitWs {
