@@ -25,10 +25,13 @@
 
 namespace bed {
 
-template <int NMAX>
+// EXACT = n equals the tier's NMAX.  At n = 32 four rows per fold thread
+// (LF = 8) beat two (65 536 matrices: 1.121 -> 1.096 ms) but not for the padded
+// n = 25..31 (1.124 -> 1.152 ms at n = 26), which keep two.
+template <int NMAX, bool EXACT = true>
 struct FTParams {
-  static constexpr int LF = NMAX <= 16 ? 4 : (NMAX <= 24 ? 6 : (NMAX <= 32 ? 16 : 32));
-  static constexpr int R = NMAX / LF;     // rows per fold thread: 4, 4, 2, 2
+  static constexpr int LF = NMAX <= 16 ? 4 : (NMAX <= 24 ? 6 : (NMAX <= 32 ? (EXACT ? 8 : 16) : 32));
+  static constexpr int R = NMAX / LF;     // rows per fold thread: 4, 4, 4 (2 padded), 2
   static constexpr int RP = (R + 1) / 2;  // packed row pairs (R = 1: scalar rows)
   static constexpr int MPC = NMAX <= 16 ? 32 : (NMAX <= 32 ? 16 : 8);
   static constexpr int FT = MPC * LF;
@@ -63,11 +66,11 @@ struct FTParams {
 // Each entry sums fma(V[r][k] V[c][k], f_k) in k order, which is symmetric in
 // (r, c), so the output is exactly symmetric (solver.py:141).
 template <int NMAX, bool EXACT, bool POW = false>
-__global__ void __launch_bounds__(FTParams<NMAX>::THREADS, FTParams<NMAX>::MINB)
+__global__ void __launch_bounds__(FTParams<NMAX, EXACT>::THREADS, FTParams<NMAX, EXACT>::MINB)
     bed_fold_tma_kernel(int64_t bc, int64_t c0, int n_rt, SplitWs ws, float* __restrict__ evals,
                         float* __restrict__ evecs, KernelCfg cfg, PowSpec pw = PowSpec{},
                         int32_t* __restrict__ status_out = nullptr, int32_t* __restrict__ flags = nullptr) {
-  using P = FTParams<NMAX>;
+  using P = FTParams<NMAX, EXACT>;
   constexpr int LF = P::LF, R = P::R, RP = P::RP, MPC = P::MPC, NB = P::NB, POS = P::POS;
   const int n = EXACT ? NMAX : n_rt;
   const int nn = n * n;

@@ -43,7 +43,7 @@ template <int NMAX, bool EXACT>
 cudaError_t launch_qf(const FwdArgs& a, const SplitWs& ws, int64_t c0, int64_t bc, cudaStream_t st) {
   const int n = a.n;
   if (a.evecs != nullptr) {
-    using FP = FTParams<NMAX>;
+    using FP = FTParams<NMAX, EXACT>;
     bed_qr_kernel<NMAX, EXACT, true><<<(unsigned)((bc + kQThreads - 1) / kQThreads), kQThreads, 0, st>>>(
         bc, c0, n, ws, a.evals, a.status, a.steps, a.flags, a.cfg, a.dg);
     if (a.pw)  // spectral power in the fold's epilogue (V never reaches memory)
@@ -68,8 +68,8 @@ cudaError_t run_split(const FwdArgs& a) {
   using HP = HHParams<NMAX>;
   cudaError_t e = ensure_smem(vecs ? bed_hh_kernel<NMAX, EXACT, true> : bed_hh_kernel<NMAX, EXACT, false>,
                               HP::BYTES);
-  if (e == cudaSuccess && vecs) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT>, FTParams<NMAX>::BYTES);
-  if (e == cudaSuccess && a.pw) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT, true>, FTParams<NMAX>::BYTES);
+  if (e == cudaSuccess && vecs) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT>, FTParams<NMAX, EXACT>::BYTES);
+  if (e == cudaSuccess && a.pw) e = ensure_smem(bed_fold_tma_kernel<NMAX, EXACT, true>, FTParams<NMAX, EXACT>::BYTES);
   if (e != cudaSuccess) return e;
   char* base = static_cast<char*>(a.ws);
 
