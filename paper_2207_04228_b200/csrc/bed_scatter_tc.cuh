@@ -25,7 +25,7 @@ struct ScatTcParams {
   static constexpr int OFF_BAR = OFF_PART + 6 * 64 * 4;
   static constexpr int OFF_TMEM = OFF_BAR + 8;
   static constexpr size_t BYTES = OFF_TMEM + 8;
-  static constexpr int CTAS_PER_SM = 3;
+  static constexpr int CTAS_PER_SM = 4;
   static constexpr int SPITCH = 65;             // S stage row pitch (in the Y region)
   static_assert(64 * SPITCH * 4 <= 2 * BUF, "stage fits in the chunk buffer");
 };
