@@ -101,8 +101,14 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
   }
   // ---- coalesced loads of V and gV into the stage, eigenvalues
   // (the generic copy targets one buffer per matrix at stride PER)
-  tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
-  if (gV) tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(gV + base * nn, count, n, smem + 2 * P::SBUF);
+  // V and gV: every 16-byte word in flight at once (cp.async) when the tile allows
+  const bool av = tile_to_stage_async<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
+  const bool ag = gV ? tile_to_stage_async<NMAX, P::THREADS, SROW, P::PER>(gV + base * nn, count, n,
+                                                                           smem + 2 * P::SBUF)
+                     : true;
+  cp_async_commit();
+  if (!av) tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
+  if (!ag) tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(gV + base * nn, count, n, smem + 2 * P::SBUF);
   for (int g = tid; g < count * n; g += P::THREADS) {
     const int mat = g / n, c = g - mat * n;
     const float l = __ldg(lam + base * n + g);
@@ -110,6 +116,7 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
     dl[c] = l;
     dl[NMAX + c] = l != 0.0f ? 1.0f / l : 0.0f;
   }
+  cp_async_wait_all();
   __syncthreads();
   for (int g = tid; g < P::MB; g += P::THREADS) outside[g] = 0;
   // V^T from V

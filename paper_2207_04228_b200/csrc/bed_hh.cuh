@@ -148,7 +148,12 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       for (int g = tid; g < G * P::SMAT; g += P::THREADS) smem[g] = 0.0f;
       __syncthreads();
     }
-    tile_to_stage<NMAX, P::THREADS, SROW, P::SMAT>(A + j0 * nn, count, n, smem);
+    if (tile_to_stage_async<NMAX, P::THREADS, SROW, P::SMAT>(A + j0 * nn, count, n, smem)) {
+      cp_async_commit();
+      cp_async_wait_all();
+    } else {
+      tile_to_stage<NMAX, P::THREADS, SROW, P::SMAT>(A + j0 * nn, count, n, smem);
+    }
   }
   __syncthreads();
 

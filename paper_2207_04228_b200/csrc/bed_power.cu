@@ -59,7 +59,9 @@ __global__ void __launch_bounds__(PowParams<NMAX>::THREADS)
     for (int g = tid; g < P::MB * P::PER; g += P::THREADS) smem[g] = 0.0f;
     __syncthreads();
   }
-  tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
+  const bool vasync = tile_to_stage_async<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
+  cp_async_commit();
+  if (!vasync) tile_to_stage<NMAX, P::THREADS, SROW, P::PER>(V + base * nn, count, n, smem);
   // f per eigenvalue; one thread per matrix resolves the floor and the
   // positivity check (n <= 64 values)
   if (t == 0 && mi < count) {
@@ -81,6 +83,7 @@ __global__ void __launch_bounds__(PowParams<NMAX>::THREADS)
     if (status && (flag || !merge)) status[base + mi] = flag ? kStatusNonPositive : kStatusOk;
     if (flag && flags) atomicOr(flags, 1 << kStatusNonPositive);
   }
+  cp_async_wait_all();
   __syncthreads();
   // V^T and diag(f) V^T from V
   for (int g = tid; g < P::MB * NMAX * NMAX; g += P::THREADS) {

@@ -76,6 +76,25 @@ __device__ __forceinline__ void tile_to_stage(const float* __restrict__ src, int
   }
 }
 
+// Asynchronous form of the fast path (cp.async, 16 bytes per copy): every
+// word of the tile is in flight at once and no register holds it; the caller
+// commits and waits (cp_async_commit / cp_async_wait_all + a barrier).
+// Returns false when the fast path does not apply (the caller falls back).
+template <int NMAX, int THREADS, int SROW, int SMAT>
+__device__ __forceinline__ bool tile_to_stage_async(const float* __restrict__ src, int count, int n,
+                                                    float* stage) {
+  static_assert(SROW % 4 == 0 && SMAT % 4 == 0, "16-byte stage rows");
+  if (!(n == NMAX && NMAX % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0)) return false;
+  constexpr int NN4 = NMAX * NMAX / 4;
+  const int total = count * NN4;
+  for (int i4 = threadIdx.x; i4 < total; i4 += THREADS) {
+    const int mat = i4 / NN4, off = (i4 - mat * NN4) * 4;
+    const int r = off / NMAX, c = off - r * NMAX;
+    cp_async_bytes<16>(stage + mat * SMAT + r * SROW + c, src + 4 * (int64_t)i4);
+  }
+  return true;
+}
+
 // The reverse copy; column c of matrix `mat` is multiplied by
 // colscale[mat * NMAX + c] when colscale is given (sign normalisation).
 template <int NMAX, int THREADS, int SROW, int SMAT>
