@@ -223,6 +223,9 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
   auto hh_step = [&](const int i, auto k0c, auto k1c, auto c0c, auto ncc) {
     constexpr int K0 = decltype(k0c)::value, K1 = decltype(k1c)::value;
     constexpr int C0 = decltype(c0c)::value, NC = decltype(ncc)::value;
+    // row groups rr < RR0 hold only rows < C0 <= i: u, p, q vanish there and
+    // the update leaves them unchanged, so their FMA work is skipped
+    constexpr int RR0 = C0 / L;
     float x[R];
     float ss = 0.0f;
 #pragma unroll
@@ -267,13 +270,17 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         for (int k = k0; k < NP; k += 2) {
           const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) {
+          for (int rr = RR0; rr < R; ++rr) {
             acc0[rr] = ffma2(a[rr][k], f2_make(u4.x, u4.y), acc0[rr]);
             if (k + 1 < NP) acc1[rr] = ffma2(a[rr][k + 1], f2_make(u4.z, u4.w), acc1[rr]);
           }
         }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
+          if (rr < RR0) {
+            p[rr] = 0.0f;
+            continue;
+          }
           const f2 acc = fadd2(acc0[rr], acc1[rr]);
           p[rr] = 2.0f * (f2_lo(acc) + f2_hi(acc));
           kk = fmaf(u[rr], p[rr], kk);
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       float q[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        q[rr] = (l + L * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
+        q[rr] = (rr >= RR0 && l + L * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
         if (l + L * rr < NMAX) qv[l + L * rr] = q[rr];
       }
       grp.sync();
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
         const float4 q4 = *reinterpret_cast<const float4*>(qv + 2 * k);
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
+        for (int rr = RR0; rr < R; ++rr) {
           a[rr][k] = ffma2(f2_bc(-u[rr]), f2_make(q4.x, q4.y),
                            ffma2(f2_bc(-q[rr]), f2_make(u4.x, u4.y), a[rr][k]));
           if (k + 1 < NP)
