@@ -359,32 +359,39 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
   }
 
   if constexpr (VECS) {
-    // ---- P = H_0 H_1 ... (householder.py:216-231), rows in registers:
-    // V <- V (I - 2 u u^T) touches columns > i only
+    // ---- P = H_0 H_1 ... H_{n-3} (householder.py:216-231), accumulated as
+    // W = P^T = H_{n-3} ... H_0 in reverse order, rows in registers:
+    // W <- W (I - 2 u u^T).  With the later reflectors applied first, W is the
+    // identity outside rows / columns > i when H_i arrives, so only those rows
+    // (row groups rr >= RR0) and columns change -- ~2/3 of the forward
+    // accumulation's FMA work; W^T is written to the stage below.  At one row
+    // per lane (n = 64) no row group ever drops out and P accumulates forward.
+    constexpr bool REV = R > 1;
     f2 v[R][NP];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         v[rr][k] = f2_make(l + L * rr == 2 * k ? 1.0f : 0.0f, l + L * rr == 2 * k + 1 ? 1.0f : 0.0f);
-    auto p_step = [&](const int i, auto k0c) {
+    auto p_step = [&](const int i, auto k0c, auto rr0c) {
       const float* urow = st + i * SROW;
       constexpr int k0 = decltype(k0c)::value;
+      constexpr int RR0 = decltype(rr0c)::value;  // row groups below: rows <= i, unchanged
       f2 acc0[R], acc1[R];
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = f2_bc(0.0f);
+      for (int rr = RR0; rr < R; ++rr) acc0[rr] = acc1[rr] = f2_bc(0.0f);
 #pragma unroll
       for (int k = k0; k < NP; k += 2) {
         const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
+        for (int rr = RR0; rr < R; ++rr) {
           acc0[rr] = ffma2(v[rr][k], f2_make(u4.x, u4.y), acc0[rr]);
           if (k + 1 < NP) acc1[rr] = ffma2(v[rr][k + 1], f2_make(u4.z, u4.w), acc1[rr]);
         }
       }
       float t[R];
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
+      for (int rr = RR0; rr < R; ++rr) {
         const f2 acc = fadd2(acc0[rr], acc1[rr]);
         t[rr] = -2.0f * (f2_lo(acc) + f2_hi(acc));
       }
@@ -392,38 +399,48 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       for (int k = k0; k < NP; k += 2) {
         const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
+        for (int rr = RR0; rr < R; ++rr) {
           v[rr][k] = ffma2(f2_bc(t[rr]), f2_make(u4.x, u4.y), v[rr][k]);
           if (k + 1 < NP) v[rr][k + 1] = ffma2(f2_bc(t[rr]), f2_make(u4.z, u4.w), v[rr][k + 1]);
         }
       }
     };
     if constexpr (kHHGroupSteps<NMAX>) {
-      static_for<0, (NMAX - 2 + 3) / 4>([&](auto gc) {
-        constexpr int g = decltype(gc)::value;
+      constexpr int NG = (NMAX - 2 + 3) / 4;
+      static_for<0, NG>([&](auto gc) {
+        constexpr int g = REV ? NG - 1 - decltype(gc)::value : decltype(gc)::value;
 #pragma unroll 1
-        for (int t = 0; t < 4; ++t) {
-          const int i = 4 * g + t;
-          if (i >= NMAX - 2 || (!EXACT && i >= n - 2)) break;
-          p_step(i, std::integral_constant<int, 2 * g>{});
+        for (int tt = 0; tt < 4; ++tt) {
+          const int i = 4 * g + (REV ? 3 - tt : tt);
+          if (i >= NMAX - 2 || (!EXACT && i >= n - 2)) continue;
+          p_step(i, std::integral_constant<int, 2 * g>{}, std::integral_constant<int, REV ? (4 * g + 1) / L : 0>{});
         }
       });
     } else {
       static_for<0, NMAX - 2>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
+        constexpr int i = REV ? NMAX - 3 - decltype(ic)::value : decltype(ic)::value;
         if (!EXACT && i >= n - 2) return;
-        p_step(i, std::integral_constant<int, ((i + 1) / 2) & ~1>{});
+        p_step(i, std::integral_constant<int, ((i + 1) / 2) & ~1>{}, std::integral_constant<int, REV ? (i + 1) / L : 0>{});
       });
     }
     grp.sync();  // every lane is done reading reflectors
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (l + L * rr >= NMAX) continue;
-      float4* r4 = reinterpret_cast<float4*>(st + (l + L * rr) * SROW);
+      if constexpr (REV) {  // P = W^T: row r of W is column r of P
+        float* col = st + l + L * rr;
 #pragma unroll
-      for (int k4 = 0; k4 < NMAX / 4; ++k4)
-        r4[k4] = make_float4(f2_lo(v[rr][2 * k4]), f2_hi(v[rr][2 * k4]), f2_lo(v[rr][2 * k4 + 1]),
-                             f2_hi(v[rr][2 * k4 + 1]));
+        for (int k = 0; k < NP; ++k) {
+          col[(2 * k) * SROW] = f2_lo(v[rr][k]);
+          col[(2 * k + 1) * SROW] = f2_hi(v[rr][k]);
+        }
+      } else {
+        float4* r4 = reinterpret_cast<float4*>(st + (l + L * rr) * SROW);
+#pragma unroll
+        for (int k4 = 0; k4 < NMAX / 4; ++k4)
+          r4[k4] = make_float4(f2_lo(v[rr][2 * k4]), f2_hi(v[rr][2 * k4]), f2_lo(v[rr][2 * k4 + 1]),
+                               f2_hi(v[rr][2 * k4 + 1]));
+      }
     }
     __syncthreads();
     stage_to_tile<NMAX, P::THREADS, SROW, P::SMAT>(smem, count, n, ws.P + j0 * nn);
