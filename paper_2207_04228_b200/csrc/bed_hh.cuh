@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     // row groups rr < RR0 hold only rows < C0 <= i: u, p, q vanish there and
     // the update leaves them unchanged, so their FMA work is skipped
     constexpr int RR0 = C0 / L;
+    // n = 64 (one row per lane, two warps): warp 0's rows drop out from i = 32
+    const bool wdead = L == 64 && C0 >= 32 && l < 32;
     float x[R];
     float ss = 0.0f;
 #pragma unroll
@@ -266,18 +268,20 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         f2 acc0[R], acc1[R];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = f2_bc(0.0f);
+        if (!wdead) {
 #pragma unroll
-        for (int k = k0; k < NP; k += 2) {
-          const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
+          for (int k = k0; k < NP; k += 2) {
+            const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
 #pragma unroll
-          for (int rr = RR0; rr < R; ++rr) {
-            acc0[rr] = ffma2(a[rr][k], f2_make(u4.x, u4.y), acc0[rr]);
-            if (k + 1 < NP) acc1[rr] = ffma2(a[rr][k + 1], f2_make(u4.z, u4.w), acc1[rr]);
+            for (int rr = RR0; rr < R; ++rr) {
+              acc0[rr] = ffma2(a[rr][k], f2_make(u4.x, u4.y), acc0[rr]);
+              if (k + 1 < NP) acc1[rr] = ffma2(a[rr][k + 1], f2_make(u4.z, u4.w), acc1[rr]);
+            }
           }
         }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
-          if (rr < RR0) {
+          if (rr < RR0 || wdead) {
             p[rr] = 0.0f;
             continue;
           }
@@ -290,14 +294,14 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
       float q[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        q[rr] = (rr >= RR0 && l + L * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
+        q[rr] = (rr >= RR0 && !wdead && l + L * rr >= i) ? fmaf(-kk, u[rr], p[rr]) : 0.0f;
         if (l + L * rr < NMAX) qv[l + L * rr] = q[rr];
       }
       grp.sync();
       // A <- A - q u^T - u q^T on columns >= i (u, q vanish on the rest)
       constexpr int k1 = K1;
 #pragma unroll
-      for (int k = k1; k < NP; k += 2) {
+      for (int k = k1; k < NP && !wdead; k += 2) {
         const float4 u4 = *reinterpret_cast<const float4*>(urow + 2 * k);
         const float4 q4 = *reinterpret_cast<const float4*>(qv + 2 * k);
 #pragma unroll
@@ -365,15 +369,16 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
     // identity outside rows / columns > i when H_i arrives, so only those rows
     // (row groups rr >= RR0) and columns change -- ~2/3 of the forward
     // accumulation's FMA work; W^T is written to the stage below.  At one row
-    // per lane (n = 64) no row group ever drops out and P accumulates forward.
-    constexpr bool REV = R > 1;
+    // per lane (n = 64) warp 0's rows drop out from i = 31.
+    constexpr bool REV = true;
     f2 v[R][NP];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         v[rr][k] = f2_make(l + L * rr == 2 * k ? 1.0f : 0.0f, l + L * rr == 2 * k + 1 ? 1.0f : 0.0f);
-    auto p_step = [&](const int i, auto k0c, auto rr0c) {
+    auto p_step = [&](const int i, auto k0c, auto rr0c, bool wdead) {
+      if (wdead) return;
       const float* urow = st + i * SROW;
       constexpr int k0 = decltype(k0c)::value;
       constexpr int RR0 = decltype(rr0c)::value;  // row groups below: rows <= i, unchanged
@@ -413,14 +418,16 @@ __global__ void __launch_bounds__(HHParams<NMAX>::THREADS, HHParams<NMAX>::MINB)
         for (int tt = 0; tt < 4; ++tt) {
           const int i = 4 * g + (REV ? 3 - tt : tt);
           if (i >= NMAX - 2 || (!EXACT && i >= n - 2)) continue;
-          p_step(i, std::integral_constant<int, 2 * g>{}, std::integral_constant<int, REV ? (4 * g + 1) / L : 0>{});
+          p_step(i, std::integral_constant<int, 2 * g>{}, std::integral_constant<int, REV ? (4 * g + 1) / L : 0>{},
+                 L == 64 && 4 * g >= 31 && l < 32);
         }
       });
     } else {
       static_for<0, NMAX - 2>([&](auto ic) {
         constexpr int i = REV ? NMAX - 3 - decltype(ic)::value : decltype(ic)::value;
         if (!EXACT && i >= n - 2) return;
-        p_step(i, std::integral_constant<int, ((i + 1) / 2) & ~1>{}, std::integral_constant<int, REV ? (i + 1) / L : 0>{});
+        p_step(i, std::integral_constant<int, ((i + 1) / 2) & ~1>{}, std::integral_constant<int, REV ? (i + 1) / L : 0>{},
+               L == 64 && i >= 31 && l < 32);
       });
     }
     grp.sync();  // every lane is done reading reflectors
