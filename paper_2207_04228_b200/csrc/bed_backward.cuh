@@ -130,98 +130,100 @@ __global__ void __launch_bounds__(BwdParams<NMAX>::THREADS)
 
   const bool live = mi < count;
   f2 acc[4][2];
-  // ---- M = V^T gV, then M' = F o M + diag(gL) in the epilogue
+  // The three products share one copy of the tile GEMM (a runtime loop keeps
+  // the kernel's code inside the instruction cache):
+  //   ph 0: M = V^T gV, then M' = F o M + diag(gL) in the epilogue
+  //   ph 1: W = V M' (A = V, read k-major from V^T); W^T goes to sV
+  //   ph 2: G = W V^T (A = W, k-major from W^T; B(j, c) = V(c, j) = V^T row j)
+#pragma unroll 1
+  for (int ph = 0; ph < 3; ++ph) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
-  if (gV) tile_gemm<NMAX, SROW>(sV, sX, ti, tj, acc);
-  // F by Horner in packed pairs (two tile columns per FFMA2)
-  float mp[4][4];
-  bool off_domain = false;
-  // a tile whose eight eigenvalues are all positive is inside the series'
-  // domain (0 < l_small <= l_big): no per-pair check
-  float tmin = sL[4 * ti];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) tmin = fminf(tmin, fminf(sL[4 * ti + q], sL[4 * tj + q]));
-  const bool tile_pos = tmin > 0.0f;
-#pragma unroll
-  for (int ii = 0; ii < 4; ++ii) {
-    const int i = 4 * ti + ii;
-    const float li = sL[i], ii_inv = sI[i];
-    const float gli = (gL && i < n && ti == tj && live) ? __ldg(gL + (base + mi) * n + i) : 0.0f;
-#pragma unroll
-    for (int jp = 0; jp < 2; ++jp) {
-      float ratio[2], binv[2];
-      bool hf[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 4 * tj + 2 * jp + h;
-        const float lj = sL[j];
-        hf[h] = i < j ? (li >= lj) : (li > lj);
-        binv[h] = hf[h] ? ii_inv : sI[j];
-        ratio[h] = (hf[h] ? lj : li) * binv[h];
-      }
-      const f2 rt = f2_make(ratio[0], ratio[1]);
-      f2 poly = f2_bc(1.0f);
-      for (int k = 0; k < degree; ++k) poly = ffma2(poly, rt, f2_bc(1.0f));
-      const f2 tt = fmul2(poly, f2_make(binv[0], binv[1]));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = 2 * jp + h, j = 4 * tj + jj;
-        float tv = h ? f2_hi(tt) : f2_lo(tt);
-        if (!tile_pos) {
-          // the series' domain: l_big > 0 and |ratio| < 1, or a tie (ratio 1)
-          const float lj = sL[j];
-          const float big = hf[h] ? li : lj, small = hf[h] ? lj : li;
-          const bool in_domain = (big > 0.0f && (fabsf(ratio[h]) < 1.0f || small == big)) ||
-                                 (big == 0.0f && small == 0.0f);
-          if (!in_domain && i != j && i < n && j < n) {
-            tv = big != small ? 1.0f / (big - small) : 0.0f;  // exact 1/(l_j - l_i), sign below
-            off_domain = true;
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
+    if (ph > 0 || gV) tile_gemm<NMAX, SROW>(ph == 1 ? sT : sV, ph == 2 ? sT : sX, ti, tj, acc);
+    if (ph == 0) {
+      // F by Horner in packed pairs (two tile columns per FFMA2)
+      float mp[4][4];
+      bool off_domain = false;
+      // a tile whose eight eigenvalues are all positive is inside the series'
+      // domain (0 < l_small <= l_big): no per-pair check
+      float tmin = sL[4 * ti];
+    #pragma unroll
+      for (int q = 0; q < 4; ++q) tmin = fminf(tmin, fminf(sL[4 * ti + q], sL[4 * tj + q]));
+      const bool tile_pos = tmin > 0.0f;
+    #pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int i = 4 * ti + ii;
+        const float li = sL[i], ii_inv = sI[i];
+        const float gli = (gL && i < n && ti == tj && live) ? __ldg(gL + (base + mi) * n + i) : 0.0f;
+    #pragma unroll
+        for (int jp = 0; jp < 2; ++jp) {
+          float ratio[2], binv[2];
+          bool hf[2];
+    #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 4 * tj + 2 * jp + h;
+            const float lj = sL[j];
+            hf[h] = i < j ? (li >= lj) : (li > lj);
+            binv[h] = hf[h] ? ii_inv : sI[j];
+            ratio[h] = (hf[h] ? lj : li) * binv[h];
+          }
+          const f2 rt = f2_make(ratio[0], ratio[1]);
+          f2 poly = f2_bc(1.0f);
+          for (int k = 0; k < degree; ++k) poly = ffma2(poly, rt, f2_bc(1.0f));
+          const f2 tt = fmul2(poly, f2_make(binv[0], binv[1]));
+    #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jj = 2 * jp + h, j = 4 * tj + jj;
+            float tv = h ? f2_hi(tt) : f2_lo(tt);
+            if (!tile_pos) {
+              // the series' domain: l_big > 0 and |ratio| < 1, or a tie (ratio 1)
+              const float lj = sL[j];
+              const float big = hf[h] ? li : lj, small = hf[h] ? lj : li;
+              const bool in_domain = (big > 0.0f && (fabsf(ratio[h]) < 1.0f || small == big)) ||
+                                     (big == 0.0f && small == 0.0f);
+              if (!in_domain && i != j && i < n && j < n) {
+                tv = big != small ? 1.0f / (big - small) : 0.0f;  // exact 1/(l_j - l_i), sign below
+                off_domain = true;
+              }
+            }
+            const float f = i == j ? 0.0f : (hf[h] ? -tv : tv);
+            mp[ii][jj] = f * tile_at(acc, ii, jj) + (i == j ? gli : 0.0f);
           }
         }
-        const float f = i == j ? 0.0f : (hf[h] ? -tv : tv);
-        mp[ii][jj] = f * tile_at(acc, ii, jj) + (i == j ? gli : 0.0f);
       }
+      if (off_domain && live) atomicOr(&outside[mi], 1);
+      __syncthreads();  // every thread is done reading gV
+      if (t == 0 && live) {
+        const int st = outside[mi] ? kStatusNonPositive : kStatusOk;
+        if (status_out) status_out[base + mi] = st;
+        if (flags && st) atomicOr(flags, 1 << st);
+      }
+      if (live) {
+    #pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+          *reinterpret_cast<float4*>(sX + (4 * ti + ii) * SROW + 4 * tj) =
+              make_float4(mp[ii][0], mp[ii][1], mp[ii][2], mp[ii][3]);
+      }
+      __syncthreads();
+
+    } else if (ph == 1) {
+      if (live) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+          *reinterpret_cast<float4*>(sV + (4 * tj + jj) * SROW + 4 * ti) =
+              make_float4(tile_at(acc, 0, jj), tile_at(acc, 1, jj), tile_at(acc, 2, jj), tile_at(acc, 3, jj));
+      }
+      __syncthreads();
+    } else {
+      if (live) {  // sX (M') was last read by the W product, before the barrier
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+          *reinterpret_cast<float4*>(sX + (4 * ti + ii) * SROW + 4 * tj) =
+              make_float4(tile_at(acc, ii, 0), tile_at(acc, ii, 1), tile_at(acc, ii, 2), tile_at(acc, ii, 3));
+      }
+      __syncthreads();
     }
   }
-  if (off_domain && live) atomicOr(&outside[mi], 1);
-  __syncthreads();  // every thread is done reading gV
-  if (t == 0 && live) {
-    const int st = outside[mi] ? kStatusNonPositive : kStatusOk;
-    if (status_out) status_out[base + mi] = st;
-    if (flags && st) atomicOr(flags, 1 << st);
-  }
-  if (live) {
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-      *reinterpret_cast<float4*>(sX + (4 * ti + ii) * SROW + 4 * tj) =
-          make_float4(mp[ii][0], mp[ii][1], mp[ii][2], mp[ii][3]);
-  }
-  __syncthreads();
-
-  // ---- W = V M' (A = V, read k-major from V^T); W^T goes to sV
-#pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
-  tile_gemm<NMAX, SROW>(sT, sX, ti, tj, acc);
-  if (live) {
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-      *reinterpret_cast<float4*>(sV + (4 * tj + jj) * SROW + 4 * ti) =
-          make_float4(tile_at(acc, 0, jj), tile_at(acc, 1, jj), tile_at(acc, 2, jj), tile_at(acc, 3, jj));
-  }
-  __syncthreads();
-
-  // ---- G = W V^T (A = W, k-major from W^T; B(j, c) = V(c, j) = V^T row j)
-#pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bc(0.0f);
-  tile_gemm<NMAX, SROW>(sV, sT, ti, tj, acc);
-  if (live) {  // sX (M') was last read by the W product, before the barrier
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-      *reinterpret_cast<float4*>(sX + (4 * ti + ii) * SROW + 4 * tj) =
-          make_float4(tile_at(acc, ii, 0), tile_at(acc, ii, 1), tile_at(acc, ii, 2), tile_at(acc, ii, 3));
-  }
-  __syncthreads();
   // ---- gA = (G + G^T) / 2, coalesced
   for (int g = tid; g < count * nn; g += P::THREADS) {
     const int mat = g / nn, off = g - mat * nn;
