@@ -37,7 +37,7 @@ struct FTParams {
   static constexpr int FT = MPC * LF;
   static constexpr int THREADS = FT + 32;  // + the producer warp
   static constexpr int MINB = NMAX <= 24 ? 4 : (NMAX <= 32 ? 2 : 1);
-  static constexpr int NB = 6;
+  static constexpr int NB = NMAX >= 32 ? 8 : 6;  // 8 fits inside the sort stage at n >= 32
   static constexpr int NW = FT / 32;   // fold warps
   static constexpr int BLK = fold_blk<NMAX>();  // positions per fold block (one branch, loads hoisted)
   static constexpr int POS = NMAX - 1;
